@@ -1,0 +1,169 @@
+/*
+ * tsv_b200.h — C ABI of the B200-native online stage of MORE-Stress
+ * (reduced global solve + per-block stress recovery).
+ *
+ * Plain pointers and sizes only; no exceptions and no torch/CUDA types
+ * cross this boundary. Every entry point names the reference interface it
+ * replaces (tsvstress, /root/reference/proj). One context owns all device
+ * memory and one CUDA stream on one GPU; a context is not thread-safe, but
+ * separate contexts may be used concurrently.
+ *
+ * Status codes mirror the reference's exception types (core.hpp:14-16,
+ * linalg.hpp:137-141, linalg.cpp:333-334): see tsv_status.
+ */
+#ifndef TSV_B200_H
+#define TSV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSV_B200_ABI_VERSION 1
+
+typedef struct tsv_ctx tsv_ctx;
+
+typedef enum {
+    TSV_OK = 0,
+    TSV_EINVAL = 1,      /* tsvstress::Error from validation (e.g. ArrayLayout::validate, global_stage.cpp:8-15) */
+    TSV_ENOCONV = 2,     /* linalg::NoConvergence (linalg.hpp:137-141); best iterate returned */
+    TSV_EBREAKDOWN = 3,  /* "NaN/Inf breakdown" / "p'Ap <= 0" (linalg.cpp:217, :333-334) */
+    TSV_ECUDA = 4,       /* CUDA runtime failure */
+    TSV_ENOMEM = 5,      /* device allocation failed */
+    TSV_ESTATE = 6       /* call order violated (e.g. solve before set_layout) */
+} tsv_status;
+
+typedef enum { /* linalg::Precond, linalg.hpp:117 */
+    TSV_PRECOND_NONE = 0,
+    TSV_PRECOND_DIAGONAL = 1,
+    TSV_PRECOND_BLOCK_DIAGONAL = 2
+} tsv_precond;
+
+typedef enum { TSV_KIND_TSV = 0, TSV_KIND_DUMMY = 1 } tsv_block_kind; /* BlockKind, mesh.hpp:43 */
+
+typedef enum { /* recovery points per element (new; the reference only samples a cut plane) */
+    TSV_POINTS_CENTROID = 1,
+    TSV_POINTS_GAUSS8 = 8
+} tsv_points;
+
+typedef enum { /* boundary conditions of the reduced system */
+    TSV_BC_BOTTOM_PIN = 0,      /* configs, literal: u_z = 0 on gz = 0, corner (0,0,0) pinned */
+    TSV_BC_BOTTOM_PIN_321 = 1,  /* + u_y = 0 at lattice (lat_x-1, 0, 0) (3-2-1 rule, SPD) */
+    TSV_BC_CLAMPED = 2,         /* GlobalBC::clamped(), global_stage.cpp:159-163 */
+    TSV_BC_NONE = 3
+} tsv_bc_kind;
+
+/* One reduced-order model (rom::ReducedOrderModel, rom.hpp:57-72) plus the
+ * unit-block mesh data recovery needs (BlockMeshes, global.hpp:113-119).
+ * Arrays are read during tsv_set_rom only. */
+typedef struct {
+    uint32_t q[3];                   /* NodeLayout n_x, n_y, n_z (rom.hpp:18-31) */
+    double geometry[4];              /* UnitBlockGeometry d, h, t, p (mesh.hpp:17-24) */
+    uint32_t grid_len[3];            /* TensorGrid line counts (mesh.hpp:28-41) */
+    const double *grid[3];           /* TensorGrid x, y, z lines */
+    double materials[3][3];          /* MaterialTable: E, nu, alpha per MaterialId (material.hpp:17-47) */
+    const uint8_t *element_material; /* cells MaterialId (mesh.cpp:182-190); NULL = rebuild from geometry */
+    const double *a_element;         /* K_r: n*n row-major */
+    const double *b_element;         /* n, for dT = 1 */
+    const double *basis;             /* Phi: n_fine*n row-major (rom.hpp:53-56) */
+    const double *thermal;           /* u_T: n_fine, for dT = 1 */
+    uint8_t fingerprint[32];         /* rom_fingerprint (rom.cpp:110-132); checked like RomSet::check_consistency */
+} tsv_rom_desc;
+
+typedef struct { /* linalg::IterOptions, linalg.hpp:120-129 (method fixed to CG) */
+    double tolerance;
+    int max_iterations;
+    int precond;
+} tsv_iter_options;
+
+typedef struct { /* GlobalSolution (global.hpp:91-96) + device timings */
+    int iterations;
+    double relative_residual;
+    int direct_fallback;      /* always 0: no CPU fallback on the GPU path */
+    int best_iterations;      /* on TSV_ENOCONV: iteration of the returned best iterate */
+    double solve_ms;          /* device time of the solve, CUDA events on the context stream */
+    uint64_t kernel_launches; /* kernels launched by this call */
+} tsv_solve_info;
+
+typedef struct { /* device-side timings of the last calls (CUDA events, context stream) */
+    double solve_ms, recover_ms;
+    double apply_ms_avg;      /* mean K1 (operator apply) launch in the last tsv_profile_apply */
+    uint64_t kernel_launches; /* cumulative since tsv_ctx_create */
+} tsv_timing;
+
+/* Context. */
+int tsv_ctx_create(int device, tsv_ctx **out);
+void tsv_ctx_destroy(tsv_ctx *ctx);
+const char *tsv_last_error(const tsv_ctx *ctx);
+int tsv_abi_version(void);
+
+/* RomSet slot `kind` (global.hpp:36-43): upload K_r, b_el, Phi, u_T and the
+ * element materials to HBM. */
+int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *rom);
+
+/* ArrayLayout (global.hpp:16-32) + RomSet::check_consistency (:52-80) +
+ * index_global_nodes (global_stage.cpp:94-119): builds the global index,
+ * the B x n dof map and the device-side gather/scatter tables. kinds may be
+ * NULL (all TSV); delta_t has 1 or rows*cols entries. */
+int tsv_set_layout(tsv_ctx *ctx, uint32_t rows, uint32_t cols, const uint8_t *kinds,
+                   const double *delta_t, size_t n_delta_t, double pitch, double height);
+
+/* Dirichlet data: a fem::DirichletSet (fem.hpp:22-36) given as sorted or
+ * unsorted (dof, value) pairs, or one of the tsv_bc_kind sets. Lifting
+ * follows apply_dirichlet_lifting (fem.cpp:223-260). */
+int tsv_set_dirichlet(tsv_ctx *ctx, size_t count, const uint32_t *dofs, const double *values);
+int tsv_set_bc(tsv_ctx *ctx, int bc_kind);
+
+/* Host-only (no GPU, no context): index_global_nodes + global_dof for a
+ * rows x cols array with NodeLayout q[3]. Any output may be NULL; sizes:
+ * node_of_lattice lat_x*lat_y*lat_z, lattice_of_node [nodes][3], dof_map
+ * rows*cols*n. Returns TSV_OK / TSV_EINVAL. */
+int tsv_index_global_nodes(uint32_t rows, uint32_t cols, const uint32_t q[3], uint64_t *n_dofs,
+                           uint32_t lattice[3], int32_t *node_of_lattice, uint32_t *lattice_of_node,
+                           uint32_t *dof_map);
+
+/* Introspection of GlobalIndex (global.hpp:47-62) for bit-exact checks. */
+int tsv_get_index(tsv_ctx *ctx, uint64_t *n_dofs, uint64_t *n_nodes, uint32_t lattice[3], uint32_t *n_reduced);
+int tsv_get_dof_map(tsv_ctx *ctx, uint32_t *dof_map /* B*n */);
+int tsv_get_lattice(tsv_ctx *ctx, int32_t *node_of_lattice, uint32_t *lattice_of_node /* [nodes][3] */);
+int tsv_get_constrained(tsv_ctx *ctx, uint8_t *mask /* N */);
+int tsv_get_load(tsv_ctx *ctx, double *b /* N, lifted */);
+
+/* y = A_lifted x (CsrMatrix::apply on the lifted assembled matrix,
+ * linalg.cpp:74-86), matrix-free on the GPU. Host buffers. */
+int tsv_apply(tsv_ctx *ctx, const double *x, double *y);
+
+/* solve_global (global_stage.cpp:187-205) -> cg_solve (linalg.cpp:292-362)
+ * on the GPU. u_out (N doubles, host) may be NULL: the solution stays
+ * resident for tsv_recover*. On TSV_ENOCONV u_out holds the best iterate. */
+int tsv_solve(tsv_ctx *ctx, const tsv_iter_options *opts, double *u_out, tsv_solve_info *info);
+
+/* Make u (N doubles, host) the resident solution (recovery from given data). */
+int tsv_set_solution(tsv_ctx *ctx, const double *u);
+
+/* Per-block recovery: gather_cell_values + reconstruct_block_field
+ * (global_stage.cpp:207-230) + evaluate_stress_in_element + von_mises
+ * (fem.cpp:262-316) at `points` per element, for original cells
+ * [cell_begin, cell_end). out[((c*E + e)*P + g)*7 + k], c relative to
+ * cell_begin, e = cell_id (mesh.cpp:125-127), g in (gx,gy,gz) order with gz
+ * fastest, k = xx,yy,zz,xy,yz,zx,vm. Host output. */
+int tsv_recover(tsv_ctx *ctx, int points, uint64_t cell_begin, uint64_t cell_end, double *out);
+
+/* Recover the whole array into context-owned HBM (no host copy) and read
+ * back any cell range of it. */
+int tsv_recover_resident(tsv_ctx *ctx, int points);
+int tsv_copy_stress(tsv_ctx *ctx, uint64_t cell_begin, uint64_t cell_end, double *out);
+
+/* Reconstructed fine displacement of one cell (reconstruct_block_field). */
+int tsv_block_field(tsv_ctx *ctx, uint64_t cell, double *out /* n_fine */);
+
+/* Measurement hooks: time `reps` K1 launches alone; read timings. */
+int tsv_profile_apply(tsv_ctx *ctx, int reps, double *ms_per_launch);
+int tsv_get_timing(tsv_ctx *ctx, tsv_timing *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSV_B200_H */

@@ -1,0 +1,298 @@
+"""Python mirror of the reference's online-stage API (tsvstress::global,
+proj/include/tsvstress/global.hpp:16-125, linalg.hpp:117-141), backed by
+the B200 C ABI. Names, argument meaning and error behaviour follow the
+reference so the parity tests read like its own tests:
+
+    ReducedOrderModel  rom.hpp:57-72         RomSet        global.hpp:36-43
+    ArrayLayout        global.hpp:16-32      GlobalIndex   global.hpp:47-62
+    IterOptions        linalg.hpp:120-129    GlobalSolution global.hpp:91-96
+    Error              core.hpp:14-16        NoConvergence linalg.hpp:137-141
+    GpuGlobalStage.index_global_nodes / apply_global_bcs / solve_global /
+    gather + reconstruct + evaluate_stress (recover) on one GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import native
+from .native import (TSV_EBREAKDOWN, TSV_ENOCONV, TSV_OK, IterOptionsC, RomDesc, SolveInfo, Timing)
+
+PRECOND = {"none": 0, "diagonal": 1, "block_diagonal": 2}
+BC = {"bottom_pin": 0, "bottom_pin_321": 1, "clamped": 2, "none": 3}
+POINTS = {"gauss": 8, "centroid": 1}
+
+
+class Error(RuntimeError):
+    """tsvstress::Error."""
+
+
+class BreakdownError(Error):
+    """CG breakdown: "NaN/Inf breakdown" or "p'Ap <= 0" (linalg.cpp:217, :333-334)."""
+
+
+class NoConvergence(Error):
+    """linalg::NoConvergence carrying the best iterate (linalg.hpp:137-141)."""
+
+    def __init__(self, msg, best: "GlobalSolution"):
+        super().__init__(msg)
+        self.best = best
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class ReducedOrderModel:
+    """One macro-element: K_r (a_element), b_element, Phi (basis), u_T
+    (thermal), plus the unit-block description recovery needs."""
+    q: tuple                       # NodeLayout (n_x, n_y, n_z)
+    geometry: tuple                # d, h, t, p
+    grid: tuple                    # (x, y, z) grid lines
+    materials: np.ndarray          # [3, 3] E, nu, alpha per MaterialId
+    a_element: np.ndarray = field(repr=False)
+    b_element: np.ndarray = field(repr=False)
+    basis: np.ndarray = field(repr=False)
+    thermal: np.ndarray = field(repr=False)
+    element_material: Optional[np.ndarray] = field(default=None, repr=False)
+    fingerprint: bytes = b"\0" * 32
+    kind: int = 0
+
+    @property
+    def reduced_dofs(self):
+        return self.a_element.shape[0]
+
+    @property
+    def fine_dofs(self):
+        return self.basis.shape[0]
+
+    @property
+    def cells(self):
+        return tuple(len(g) - 1 for g in self.grid)
+
+    @classmethod
+    def from_arrays(cls, obj, kind=None):
+        """From any object exposing the oracle-style attribute names
+        (K, b_el, Phi, u_T, gx, gy, gz, elem_mat, mats, geom, q, fingerprint)."""
+        return cls(q=tuple(int(v) for v in obj.q), geometry=tuple(float(v) for v in obj.geom),
+                   grid=(obj.gx, obj.gy, obj.gz), materials=np.asarray(obj.mats)[:, :3].copy(),
+                   a_element=obj.K, b_element=obj.b_el, basis=obj.Phi, thermal=obj.u_T,
+                   element_material=obj.elem_mat, fingerprint=bytes(obj.fingerprint),
+                   kind=int(obj.kind if kind is None else kind))
+
+
+@dataclass
+class ArrayLayout:
+    rows: int = 1
+    cols: int = 1
+    kinds: Optional[np.ndarray] = None     # None = all tsv; 1 = dummy
+    delta_t: Sequence[float] = (-250.0,)
+    pitch: float = 0.0
+    height: float = 0.0
+
+    @property
+    def cell_count(self):
+        return self.rows * self.cols
+
+
+@dataclass
+class IterOptions:
+    tolerance: float = 1e-10
+    max_iterations: int = 10000
+    precond: str = "diagonal"
+
+
+@dataclass
+class GlobalSolution:
+    u: Optional[np.ndarray]
+    iterations: int = 0
+    relative_residual: float = 0.0
+    direct_fallback: bool = False
+    best_iterations: int = 0
+    solve_ms: float = 0.0
+    kernel_launches: int = 0
+
+
+@dataclass
+class GlobalIndex:
+    lat_x: int
+    lat_y: int
+    lat_z: int
+    node_count: int
+    dof_count: int
+    reduced_dofs: int
+
+
+class GpuGlobalStage:
+    """One GPU context: ROMs and the array resident in HBM."""
+
+    def __init__(self, device: int = 0):
+        self._L = native.load()
+        h = C.c_void_p()
+        rc = self._L.tsv_ctx_create(device, C.byref(h))
+        if rc != TSV_OK:
+            raise Error(f"tsv_ctx_create failed with status {rc} (CUDA device {device} unavailable?)")
+        self._h = h
+        self._keep = []
+        self.layout: Optional[ArrayLayout] = None
+        self.roms = [None, None]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tsv_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -------------------------------------------------------------- errors
+    def _check(self, rc, what=""):
+        if rc == TSV_OK:
+            return
+        msg = self._L.tsv_last_error(self._h).decode()
+        if rc == TSV_EBREAKDOWN:
+            raise BreakdownError(msg)
+        raise Error(f"{what}: {msg}" if what else msg)
+
+    # ------------------------------------------------------------- set-up
+    def set_rom(self, kind: int, rom: ReducedOrderModel):
+        d = RomDesc()
+        d.q[:] = [int(v) for v in rom.q]
+        d.geometry[:] = [float(v) for v in rom.geometry]
+        grids = [np.ascontiguousarray(g, np.float64) for g in rom.grid]
+        d.grid_len[:] = [len(g) for g in grids]
+        for a in range(3):
+            d.grid[a] = _p(grids[a])
+        mats = np.asarray(rom.materials, np.float64)
+        for i in range(3):
+            for j in range(3):
+                d.materials[i][j] = float(mats[i, j])
+        em = None if rom.element_material is None else np.ascontiguousarray(rom.element_material, np.uint8)
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (rom.a_element, rom.b_element, rom.basis, rom.thermal)]
+        d.element_material = _p(em)
+        d.a_element, d.b_element, d.basis, d.thermal = [_p(a) for a in arrs]
+        d.fingerprint[:] = list(bytes(rom.fingerprint)[:32].ljust(32, b"\0"))
+        self._check(self._L.tsv_set_rom(self._h, kind, C.byref(d)), "set_rom")
+        self.roms[kind] = rom
+
+    def set_roms(self, tsv: Optional[ReducedOrderModel] = None, dummy: Optional[ReducedOrderModel] = None):
+        if tsv is not None:
+            self.set_rom(0, tsv)
+        if dummy is not None:
+            self.set_rom(1, dummy)
+
+    def set_layout(self, layout: ArrayLayout):
+        kinds = None if layout.kinds is None else np.ascontiguousarray(layout.kinds, np.uint8)
+        dt = np.ascontiguousarray(np.atleast_1d(np.asarray(layout.delta_t, np.float64)))
+        self._check(self._L.tsv_set_layout(self._h, layout.rows, layout.cols, _p(kinds), _p(dt), dt.size,
+                                           float(layout.pitch), float(layout.height)), "set_layout")
+        self.layout = layout
+
+    def set_bc(self, kind: str = "bottom_pin_321"):
+        self._check(self._L.tsv_set_bc(self._h, BC[kind]), "set_bc")
+
+    def set_dirichlet(self, dofs, values):
+        dofs = np.ascontiguousarray(dofs, np.uint32)
+        values = np.ascontiguousarray(values, np.float64)
+        self._check(self._L.tsv_set_dirichlet(self._h, dofs.size, _p(dofs), _p(values)), "set_dirichlet")
+
+    # -------------------------------------------------------------- index
+    def index(self) -> GlobalIndex:
+        nd, nn, nr = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        lat = (C.c_uint32 * 3)()
+        self._check(self._L.tsv_get_index(self._h, C.byref(nd), C.byref(nn), lat, C.byref(nr)))
+        return GlobalIndex(lat[0], lat[1], lat[2], nn.value, nd.value, nr.value)
+
+    def dof_map(self):
+        ix = self.index()
+        out = np.empty((self.layout.cell_count, ix.reduced_dofs), np.uint32)
+        self._check(self._L.tsv_get_dof_map(self._h, _p(out)))
+        return out
+
+    def lattice(self):
+        ix = self.index()
+        nol = np.empty(ix.lat_x * ix.lat_y * ix.lat_z, np.int32)
+        lon = np.empty((ix.node_count, 3), np.uint32)
+        self._check(self._L.tsv_get_lattice(self._h, _p(nol), _p(lon)))
+        return nol, lon
+
+    def constrained(self):
+        out = np.empty(self.index().dof_count, np.uint8)
+        self._check(self._L.tsv_get_constrained(self._h, _p(out)))
+        return out
+
+    def load(self):
+        out = np.empty(self.index().dof_count)
+        self._check(self._L.tsv_get_load(self._h, _p(out)))
+        return out
+
+    # ------------------------------------------------------------ compute
+    def apply(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty_like(x)
+        self._check(self._L.tsv_apply(self._h, _p(x), _p(y)), "apply")
+        return y
+
+    def solve_global(self, opts: IterOptions = IterOptions(), copy_out: bool = True) -> GlobalSolution:
+        o = IterOptionsC(float(opts.tolerance), int(opts.max_iterations), PRECOND[opts.precond])
+        info = SolveInfo()
+        u = np.empty(self.index().dof_count) if copy_out else None
+        rc = self._L.tsv_solve(self._h, C.byref(o), _p(u), C.byref(info))
+        sol = GlobalSolution(u, info.iterations, info.relative_residual, bool(info.direct_fallback),
+                             info.best_iterations, info.solve_ms, info.kernel_launches)
+        if rc == TSV_ENOCONV:
+            raise NoConvergence(self._L.tsv_last_error(self._h).decode(), sol)
+        self._check(rc, "solve_global")
+        return sol
+
+    def set_solution(self, u):
+        u = np.ascontiguousarray(u, np.float64)
+        self._check(self._L.tsv_set_solution(self._h, _p(u)), "set_solution")
+
+    def _elems(self):
+        r = self.roms[0] or self.roms[1]
+        cx, cy, cz = r.cells
+        return cx * cy * cz
+
+    def recover(self, points: int = 8, cell_begin: int = 0, cell_end: Optional[int] = None):
+        cell_end = self.layout.cell_count if cell_end is None else cell_end
+        out = np.empty((cell_end - cell_begin, self._elems(), points, 7))
+        self._check(self._L.tsv_recover(self._h, points, cell_begin, cell_end, _p(out)), "recover")
+        return out
+
+    def recover_resident(self, points: int = 8):
+        self._check(self._L.tsv_recover_resident(self._h, points), "recover_resident")
+
+    def copy_stress(self, cell_begin, cell_end, points):
+        out = np.empty((cell_end - cell_begin, self._elems(), points, 7))
+        self._check(self._L.tsv_copy_stress(self._h, cell_begin, cell_end, _p(out)), "copy_stress")
+        return out
+
+    def block_field(self, cell: int):
+        r = self.roms[0] or self.roms[1]
+        out = np.empty(r.fine_dofs)
+        self._check(self._L.tsv_block_field(self._h, cell, _p(out)), "block_field")
+        return out
+
+    def profile_apply(self, reps: int = 20) -> float:
+        ms = C.c_double()
+        self._check(self._L.tsv_profile_apply(self._h, reps, C.byref(ms)), "profile_apply")
+        return ms.value
+
+    def timing(self) -> Timing:
+        t = Timing()
+        self._check(self._L.tsv_get_timing(self._h, C.byref(t)))
+        return t

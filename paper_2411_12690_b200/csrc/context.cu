@@ -1,0 +1,1104 @@
+// tsv_ctx: device residency, the PCG driver and the recovery driver behind
+// the C ABI of include/tsv_b200.h.
+//
+// Data layout in HBM:
+//   K_r[kind]   [round_up(n, BN) rows][ldk]     zero-padded, symmetric
+//   Phi[kind]   [round_up(n_fine, BN)][ldk]     row-major fine DoF x reduced DoF
+//   X, Y        [B_pad][ldk]                    block-major operand / product panels
+//               (GEMM row j = block, blocks grouped by kind, each kind padded to BM)
+//   slots       [nodes][4] int32                offsets j*ldk + 3*rank of every
+//               (block, local node) copy of an owned global node; nodes are
+//               renumbered block-major (owner = first block in GEMM-row order)
+//   x r p ap b  [N] in that internal node order; mapped back to the
+//               reference numbering (global_stage.cpp:94-119) at the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tsv_b200.h"
+#include "host_index.hpp"
+#include "kernels.cuh"
+
+using namespace tsvb200;
+
+namespace {
+
+using K1Cfg = GemmCfg<128, 64, 2, 2, 16, 3>;
+using K6Cfg = GemmCfg<128, 64, 2, 2, 16, 3>;
+constexpr int kBM = K1Cfg::BM;
+constexpr int kBN = K1Cfg::BN;
+constexpr int kKC = K1Cfg::KC;
+constexpr int kVecThreads = 256;
+constexpr int kItersPerGraph = 16;
+
+struct StatusError : std::runtime_error {
+    StatusError(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+    int code;
+};
+
+#define CK(expr)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw StatusError(e_ == cudaErrorMemoryAllocation ? TSV_ENOMEM : TSV_ECUDA,            \
+                              std::string(#expr) + ": " + cudaGetErrorString(e_));                 \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T *ptr = nullptr;
+    size_t count = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        count = 0;
+    }
+    void alloc(size_t n) {
+        if (n == count && ptr) return;
+        release();
+        if (n == 0) return;
+        CK(cudaMalloc(&ptr, n * sizeof(T)));
+        count = n;
+    }
+    void upload(const T *src, size_t n, cudaStream_t s) {
+        alloc(n);
+        if (n) CK(cudaMemcpyAsync(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+struct RomHost {
+    bool set = false;
+    uint32_t q[3] = {0, 0, 0};
+    double geom[4] = {0, 0, 0, 0};
+    std::vector<double> grid[3];
+    double mats[3][3] = {};
+    double lame[3][3] = {};  // lambda, mu, alpha*(3 lambda + 2 mu)
+    std::vector<uint8_t> elem_mat;
+    std::vector<double> k_r, b_el, u_t;  // host copies used for assembly of b / preconditioners
+    size_t n = 0, n_fine = 0, cells[3] = {0, 0, 0};
+    uint8_t fingerprint[32] = {};
+    DevBuf<double> d_k, d_phi, d_ut, d_hinv;
+    DevBuf<uint8_t> d_em;
+};
+
+}  // namespace
+
+struct tsv_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int sm_count = 148;
+    uint64_t launches = 0;
+
+    RomHost rom[2];
+
+    // layout
+    bool layout_set = false;
+    ArrayLayout layout;
+    NodeLayout nl;
+    GlobalIndex index;
+    std::vector<uint32_t> dofmap;  // [B][n]
+    size_t n = 0, ldk = 0, B = 0, B_pad = 0, m_tiles = 0, nodes = 0, N = 0;
+    std::vector<int> row_cell, cell_row;
+    std::vector<uint8_t> row_kind, tile_kind;
+    std::vector<double> row_dt;
+    std::vector<uint32_t> node_glob_of_int, node_int_of_glob;
+
+    // boundary conditions (reference numbering)
+    bool bc_set = false;
+    std::vector<uint8_t> constrained;
+    std::vector<double> g;
+    bool any_g = false;
+
+    // device
+    DevBuf<double> X, Y, b, x, r, p, ap, pre, partial, row_dt_d, U, stress;
+    DevBuf<int> slots, row_cell_d;
+    DevBuf<uint8_t> cmask, row_kind_d, tile_kind_d;
+    DevBuf<unsigned> tile_counter;
+    DevBuf<CgState> state;
+    int pre_kind = -1;
+    bool solution_valid = false;
+    int stress_points = 0;
+    CgState *h_state = nullptr;  // pinned
+
+    cudaGraphExec_t iter_graph = nullptr;
+    int k1_grid = 0, k6_grid = 0;
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
+
+    ~tsv_ctx() {
+        if (iter_graph) cudaGraphExecDestroy(iter_graph);
+        if (h_state) cudaFreeHost(h_state);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void drop_graph() {
+        if (iter_graph) cudaGraphExecDestroy(iter_graph);
+        iter_graph = nullptr;
+    }
+
+    const RomHost &rom_of(int kind) const { return rom[kind]; }
+
+    // ------------------------------------------------------------ layout
+    void build_layout(uint32_t rows, uint32_t cols, const uint8_t *kinds, const double *dt, size_t ndt,
+                      double pitch, double height) {
+        ArrayLayout L;
+        L.rows = rows;
+        L.cols = cols;
+        if (kinds) L.kinds.assign(kinds, kinds + static_cast<size_t>(rows) * cols);
+        if (!dt && ndt) throw StatusError(TSV_EINVAL, "layout: delta_t pointer is NULL");
+        L.delta_t.assign(dt, dt + ndt);
+        L.pitch = pitch;
+        L.height = height;
+        L.validate();
+        // RomSet::check_consistency (global_stage.cpp:52-80)
+        bool need[2] = {false, false};
+        for (size_t c = 0; c < L.cell_count(); ++c) need[L.kind_at(c)] = true;
+        if (need[0] && !rom[0].set) throw StatusError(TSV_EINVAL, "layout contains tsv blocks but no tsv model is loaded");
+        if (need[1] && !rom[1].set)
+            throw StatusError(TSV_EINVAL, "layout contains dummy blocks but no dummy model is loaded");
+        if (rom[0].set && rom[1].set && std::memcmp(rom[0].fingerprint, rom[1].fingerprint, 32) != 0)
+            throw StatusError(TSV_EINVAL, "tsv and dummy models come from different parameter sets (fingerprint mismatch)");
+        const RomHost &m = rom[0].set ? rom[0] : rom[1];
+        if (!m.set) throw StatusError(TSV_EINVAL, "RomSet: no models loaded");
+        if (m.geom[3] != pitch || m.geom[1] != height)
+            throw StatusError(TSV_EINVAL, "model geometry does not match the layout pitch/height (fingerprint mismatch)");
+
+        layout = L;
+        nl = NodeLayout::create(m.q[0], m.q[1], m.q[2]);
+        index = index_global_nodes(layout, nl);
+        dofmap = tsvb200::dof_map(layout, index, nl);
+        n = nl.reduced_dofs();
+        ldk = round_up(n, kKC);
+        B = layout.cell_count();
+        N = index.dof_count();
+        nodes = index.node_count();
+
+        // GEMM row order: blocks grouped by kind, each group padded to BM rows.
+        row_cell.clear();
+        row_kind.clear();
+        row_dt.clear();
+        tile_kind.clear();
+        for (int kind = 0; kind < 2; ++kind) {
+            size_t cnt = 0;
+            for (size_t c = 0; c < B; ++c)
+                if (layout.kind_at(c) == kind) {
+                    row_cell.push_back(static_cast<int>(c));
+                    row_kind.push_back(static_cast<uint8_t>(kind));
+                    row_dt.push_back(layout.delta_t_at(c));
+                    ++cnt;
+                }
+            while (row_cell.size() % kBM) {
+                row_cell.push_back(-1);
+                row_kind.push_back(static_cast<uint8_t>(kind));
+                row_dt.push_back(0.0);
+            }
+            for (size_t t = 0; t < round_up(cnt, kBM) / kBM; ++t) tile_kind.push_back(static_cast<uint8_t>(kind));
+        }
+        B_pad = row_cell.size();
+        m_tiles = B_pad / kBM;
+        if (B_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "array too large for 32-bit panel offsets");
+        cell_row.assign(B, -1);
+        for (size_t j = 0; j < B_pad; ++j)
+            if (row_cell[j] >= 0) cell_row[row_cell[j]] = static_cast<int>(j);
+
+        // Block-major node renumbering + slot table.
+        const size_t nn = nl.node_count();
+        node_int_of_glob.assign(nodes, 0xffffffffu);
+        node_glob_of_int.clear();
+        node_glob_of_int.reserve(nodes);
+        std::vector<int> slot_tab(nodes * 4, -1);
+        for (size_t j = 0; j < B_pad; ++j) {
+            const int cell = row_cell[j];
+            if (cell < 0) continue;
+            const uint32_t *dm = dofmap.data() + static_cast<size_t>(cell) * n;
+            for (size_t rank = 0; rank < nn; ++rank) {
+                const uint32_t gnode = dm[3 * rank] / 3;
+                uint32_t &in = node_int_of_glob[gnode];
+                if (in == 0xffffffffu) {
+                    in = static_cast<uint32_t>(node_glob_of_int.size());
+                    node_glob_of_int.push_back(gnode);
+                }
+                int *s = slot_tab.data() + static_cast<size_t>(in) * 4;
+                int k = 0;
+                while (k < 4 && s[k] >= 0) ++k;
+                if (k == 4) throw StatusError(TSV_EINVAL, "index: a reduced node is shared by more than 4 blocks");
+                s[k] = static_cast<int>(j * ldk + 3 * rank);
+            }
+        }
+        if (node_glob_of_int.size() != nodes) throw StatusError(TSV_EINVAL, "index: unreferenced global node");
+
+        drop_graph();
+        solution_valid = false;
+        pre_kind = -1;
+        stress.release();
+        cudaStream_t s = stream;
+        slots.upload(slot_tab.data(), slot_tab.size(), s);
+        row_cell_d.upload(row_cell.data(), row_cell.size(), s);
+        row_kind_d.upload(row_kind.data(), row_kind.size(), s);
+        tile_kind_d.upload(tile_kind.data(), tile_kind.size(), s);
+        row_dt_d.upload(row_dt.data(), row_dt.size(), s);
+        X.alloc(B_pad * ldk);
+        Y.alloc(B_pad * ldk);
+        CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), s));
+        CK(cudaMemsetAsync(Y.ptr, 0, Y.count * sizeof(double), s));
+        for (DevBuf<double> *v : {&b, &x, &r, &p, &ap}) {
+            v->alloc(N);
+            CK(cudaMemsetAsync(v->ptr, 0, N * sizeof(double), s));
+        }
+        const size_t vec_blocks = (nodes + kVecThreads - 1) / kVecThreads;
+        partial.alloc(2 * std::max<size_t>(vec_blocks, 1));
+        layout_set = true;
+        bc_set = false;
+        set_bc_mask(std::vector<uint8_t>(N, 0), std::vector<double>(N, 0.0));
+        bc_set = false;
+        CK(cudaStreamSynchronize(s));
+    }
+
+    // ------------------------------------------------------------------ BC
+    void set_bc_mask(std::vector<uint8_t> mask, std::vector<double> vals) {
+        constrained = std::move(mask);
+        g = std::move(vals);
+        any_g = false;
+        for (size_t i = 0; i < N; ++i)
+            if (constrained[i] && g[i] != 0.0) any_g = true;
+        std::vector<uint8_t> cm_int(N);
+        for (size_t in = 0; in < nodes; ++in)
+            for (int c = 0; c < 3; ++c) cm_int[3 * in + c] = constrained[3 * node_glob_of_int[in] + c];
+        cmask.upload(cm_int.data(), N, stream);
+        bc_set = true;
+        pre_kind = -1;
+        solution_valid = false;
+        build_rhs();
+    }
+
+    template <typename T>
+    std::vector<T> to_internal(const T *v) const {
+        std::vector<T> out(N);
+        for (size_t in = 0; in < nodes; ++in)
+            for (int c = 0; c < 3; ++c) out[3 * in + c] = v[3 * node_glob_of_int[in] + c];
+        return out;
+    }
+    template <typename T>
+    void to_reference(const T *v_int, T *out) const {
+        for (size_t in = 0; in < nodes; ++in)
+            for (int c = 0; c < 3; ++c) out[3 * node_glob_of_int[in] + c] = v_int[3 * in + c];
+    }
+
+    // Assembled load (global_stage.cpp:135-142, cell order, bit-exact) and
+    // symmetric lifting (fem.cpp:223-260): b_c = g, b_f -= A_fc g.
+    void build_rhs() {
+        std::vector<double> bg(N, 0.0);
+        for (size_t c = 0; c < B; ++c) {
+            const RomHost &m = rom[layout.kind_at(c)];
+            const double dt = layout.delta_t_at(c);
+            const uint32_t *dm = dofmap.data() + c * n;
+            for (size_t a = 0; a < n; ++a) bg[dm[a]] += dt * m.b_el[a];
+        }
+        for (size_t i = 0; i < N; ++i)
+            if (constrained[i]) bg[i] = g[i];
+        std::vector<double> bi = to_internal(bg.data());
+        b.upload(bi.data(), N, stream);
+        if (any_g) {  // b_f -= A_fc g on the device
+            std::vector<double> gi = to_internal(g.data());
+            r.upload(gi.data(), N, stream);
+            launch_scatter(r.ptr, 2);
+            launch_k1(nullptr);
+            gather_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), slots.ptr, cmask.ptr,
+                                                                    Y.ptr, b.ptr, b.ptr, 1);
+            ++launches;
+            CK(cudaGetLastError());
+        }
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    // Jacobi / 3x3 block-Jacobi of the lifted matrix, built on the host in
+    // the reference's summation order (linalg.cpp:223-262).
+    void build_precond(int kind) {
+        if (pre_kind == kind) return;
+        if (kind == TSV_PRECOND_DIAGONAL) {
+            std::vector<double> d(N, 0.0);
+            for (size_t c = 0; c < B; ++c) {
+                const RomHost &m = rom[layout.kind_at(c)];
+                const uint32_t *dm = dofmap.data() + c * n;
+                for (size_t a = 0; a < n; ++a) d[dm[a]] += m.k_r[a * n + a];
+            }
+            for (size_t i = 0; i < N; ++i) {
+                if (constrained[i]) d[i] = 1.0;
+                d[i] = d[i] != 0.0 ? 1.0 / d[i] : 1.0;
+            }
+            std::vector<double> di = to_internal(d.data());
+            pre.upload(di.data(), N, stream);
+        } else if (kind == TSV_PRECOND_BLOCK_DIAGONAL) {
+            std::vector<double> mb(nodes * 9, 0.0);
+            const size_t nn = nl.node_count();
+            for (size_t c = 0; c < B; ++c) {
+                const RomHost &m = rom[layout.kind_at(c)];
+                const uint32_t *dm = dofmap.data() + c * n;
+                for (size_t rank = 0; rank < nn; ++rank) {
+                    const size_t node = dm[3 * rank] / 3;
+                    for (int i = 0; i < 3; ++i)
+                        for (int j = 0; j < 3; ++j) mb[node * 9 + i * 3 + j] += m.k_r[(3 * rank + i) * n + 3 * rank + j];
+                }
+            }
+            std::vector<double> inv_int(nodes * 9);
+            for (size_t node = 0; node < nodes; ++node) {
+                double mm[9];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) {
+                        double v = mb[node * 9 + i * 3 + j];
+                        if (constrained[3 * node + i]) v = (i == j) ? 1.0 : 0.0;
+                        else if (constrained[3 * node + j]) v = 0.0;
+                        mm[i * 3 + j] = v;
+                    }
+                const double *m = mm;
+                double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                             m[2] * (m[3] * m[7] - m[4] * m[6]);
+                double inv[9];
+                if (std::abs(det) < 1e-300) {
+                    for (int i = 0; i < 9; ++i) inv[i] = 0.0;
+                    for (int i = 0; i < 3; ++i) {
+                        double dd = m[i * 3 + i];
+                        inv[i * 3 + i] = dd != 0.0 ? 1.0 / dd : 1.0;
+                    }
+                } else {
+                    inv[0] = (m[4] * m[8] - m[5] * m[7]) / det;
+                    inv[1] = (m[2] * m[7] - m[1] * m[8]) / det;
+                    inv[2] = (m[1] * m[5] - m[2] * m[4]) / det;
+                    inv[3] = (m[5] * m[6] - m[3] * m[8]) / det;
+                    inv[4] = (m[0] * m[8] - m[2] * m[6]) / det;
+                    inv[5] = (m[2] * m[3] - m[0] * m[5]) / det;
+                    inv[6] = (m[3] * m[7] - m[4] * m[6]) / det;
+                    inv[7] = (m[1] * m[6] - m[0] * m[7]) / det;
+                    inv[8] = (m[0] * m[4] - m[1] * m[3]) / det;
+                }
+                const size_t in = node_int_of_glob[node];
+                std::memcpy(inv_int.data() + in * 9, inv, sizeof(inv));
+            }
+            pre.upload(inv_int.data(), inv_int.size(), stream);
+        } else {
+            pre.alloc(1);
+        }
+        pre_kind = kind;
+        drop_graph();
+    }
+
+    // ------------------------------------------------------------ kernels
+    unsigned vec_grid() const { return static_cast<unsigned>(std::max<size_t>(1, (nodes + kVecThreads - 1) / kVecThreads)); }
+
+    void launch_scatter(const double *v, int mode) {
+        scatter_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), slots.ptr, cmask.ptr, v,
+                                                                    X.ptr, mode);
+        ++launches;
+        CK(cudaGetLastError());
+    }
+
+    GemmParams k1_params(const int *done) {
+        GemmParams gp{};
+        gp.A = X.ptr;
+        gp.lda = static_cast<long long>(ldk);
+        gp.Bt[0] = rom[0].set ? rom[0].d_k.ptr : rom[1].d_k.ptr;
+        gp.Bt[1] = rom[1].set ? rom[1].d_k.ptr : rom[0].d_k.ptr;
+        gp.ldb = static_cast<long long>(ldk);
+        gp.tile_kind = tile_kind_d.ptr;
+        gp.C = Y.ptr;
+        gp.ldc = static_cast<long long>(ldk);
+        gp.m_tiles = static_cast<int>(m_tiles);
+        gp.n_tiles = static_cast<int>(round_up(n, kBN) / kBN);
+        gp.k_chunks = static_cast<int>(ldk / kKC);
+        gp.n_valid = static_cast<int>(n);
+        gp.n_store = static_cast<int>(n);
+        gp.row_scale = nullptr;
+        gp.done = done;
+        gp.tile_counter = tile_counter.ptr;
+        return gp;
+    }
+
+    void launch_k1(const int *done) {
+        GemmParams gp = k1_params(done);
+        gemm_nt_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp);
+        ++launches;
+        CK(cudaGetLastError());
+    }
+
+    CgParams cg_params() {
+        CgParams q{};
+        q.st = state.ptr;
+        q.n_nodes = static_cast<int>(nodes);
+        q.slots = slots.ptr;
+        q.cmask = cmask.ptr;
+        q.b = b.ptr;
+        q.x = x.ptr;
+        q.r = r.ptr;
+        q.p = p.ptr;
+        q.ap = ap.ptr;
+        q.Y = Y.ptr;
+        q.X = X.ptr;
+        q.precond = pre_kind;
+        q.pre = pre.ptr;
+        q.partial = partial.ptr;
+        return q;
+    }
+
+    void launch_iteration(const CgParams &q) {
+        launch_k1(&state.ptr->done);
+        cg_gather_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        cg_update_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        cg_scatter_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        launches += 3;
+    }
+
+    void ensure_graph() {
+        if (iter_graph) return;
+        CgParams q = cg_params();
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        const uint64_t before = launches;
+        for (int i = 0; i < kItersPerGraph; ++i) launch_iteration(q);
+        launches = before;
+        CK(cudaStreamEndCapture(stream, &graph));
+        CK(cudaGraphInstantiate(&iter_graph, graph, 0));
+        cudaGraphDestroy(graph);
+    }
+
+    // ------------------------------------------------------------- solve
+    int solve(const tsv_iter_options &o, double *u_out, tsv_solve_info *info) {
+        if (!layout_set) throw StatusError(TSV_ESTATE, "solve: no layout set");
+        if (!(o.tolerance > 0.0)) throw StatusError(TSV_EINVAL, "IterOptions: tolerance must be > 0");
+        if (o.max_iterations < 1) throw StatusError(TSV_EINVAL, "IterOptions: max_iterations must be >= 1");
+        if (o.precond < 0 || o.precond > 2) throw StatusError(TSV_EINVAL, "IterOptions: unknown preconditioner");
+        build_precond(o.precond);
+        const uint64_t l0 = launches;
+        CK(cudaEventRecord(ev0, stream));
+        CgState st = run_cg(o.tolerance, o.max_iterations);
+        int status = TSV_OK;
+        int best_it = st.it;
+        double relres = st.norm_b > 0.0 ? st.res / st.norm_b : 0.0;
+        if (st.done == CG_NOCONV) {
+            status = TSV_ENOCONV;
+            best_it = st.best_it;
+            relres = st.best_res / st.norm_b;
+            if (st.best_it < st.it) {
+                // Bitwise-deterministic replay up to the best iterate
+                // (the reference keeps a copy of it, linalg.cpp:346-349).
+                CgState st2 = run_cg(o.tolerance, st.best_it);
+                (void)st2;
+            }
+        } else if (st.done == CG_BREAKDOWN) {
+            CK(cudaEventRecord(ev1, stream));
+            CK(cudaEventSynchronize(ev1));
+            solution_valid = false;
+            throw StatusError(TSV_EBREAKDOWN, st.breakdown_code == 2
+                                                  ? "iterative_solve: matrix not positive definite for CG (p'Ap <= 0)"
+                                                  : "iterative_solve: NaN/Inf breakdown");
+        }
+        CK(cudaEventRecord(ev1, stream));
+        CK(cudaEventSynchronize(ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        last_solve_ms = ms;
+        solution_valid = true;
+        if (u_out) {
+            std::vector<double> xi(N);
+            CK(cudaMemcpy(xi.data(), x.ptr, N * sizeof(double), cudaMemcpyDeviceToHost));
+            to_reference(xi.data(), u_out);
+        }
+        if (info) {
+            info->iterations = st.it;
+            info->relative_residual = relres;
+            info->direct_fallback = 0;
+            info->best_iterations = best_it;
+            info->solve_ms = ms;
+            info->kernel_launches = launches - l0;
+        }
+        if (status == TSV_ENOCONV) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf,
+                          "iterative_solve: CG did not reach tolerance %f in %d iterations (best residual %f)",
+                          o.tolerance, st.it, relres);
+            err = buf;
+        }
+        return status;
+    }
+
+    CgState run_cg(double tol, int max_it) {
+        ensure_graph();
+        CgState s{};
+        s.done = CG_RUNNING;
+        s.phase = PH_INIT;
+        s.tol = tol;
+        s.max_it = max_it;
+        *h_state = s;
+        CK(cudaMemcpyAsync(state.ptr, h_state, sizeof(CgState), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), stream));
+        CgParams q = cg_params();
+        cg_update_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        cg_scatter_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        launches += 2;
+        CK(cudaGetLastError());
+        // Host-polled batches of graph-captured iterations; a finished
+        // solve turns the remaining launches into early exits.
+        const int graph_nodes = 4 * kItersPerGraph;
+        for (;;) {
+            CK(cudaGraphLaunch(iter_graph, stream));
+            launches += graph_nodes;
+            CK(cudaMemcpyAsync(h_state, state.ptr, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            if (h_state->done != CG_RUNNING) break;
+        }
+        return *h_state;
+    }
+
+    // ----------------------------------------------------------- recovery
+    void check_recovery(int points) {
+        if (!layout_set) throw StatusError(TSV_ESTATE, "recover: no layout set");
+        if (!solution_valid) throw StatusError(TSV_ESTATE, "recover: no solution (call tsv_solve or tsv_set_solution)");
+        if (points != 1 && points != 8) throw StatusError(TSV_EINVAL, "recover: points must be 1 (centroid) or 8 (Gauss)");
+        const RomHost &m = rom[0].set ? rom[0] : rom[1];
+        if (rom[0].set && rom[1].set)
+            for (int a = 0; a < 3; ++a)
+                if (rom[0].cells[a] != rom[1].cells[a]) throw StatusError(TSV_EINVAL, "recover: tsv/dummy meshes differ");
+        (void)m;
+    }
+
+    size_t elems() const {
+        const RomHost &m = rom[0].set ? rom[0] : rom[1];
+        return m.cells[0] * m.cells[1] * m.cells[2];
+    }
+
+    // Recover cells [c0, c1) into device buffer `out` (cells-relative).
+    void recover_range(int points, size_t c0, size_t c1, double *out) {
+        const RomHost &m = rom[0].set ? rom[0] : rom[1];
+        const size_t ldu = round_up(m.n_fine, 8);
+        // Q panel: u at every DoF of every block (gather_cell_values does not mask).
+        launch_scatter(x.ptr, 1);
+        // M tiles holding the requested cells.
+        std::vector<char> need(m_tiles, 0);
+        for (size_t c = c0; c < c1; ++c) need[cell_row[c] / kBM] = 1;
+        const size_t chunk_tiles = std::max<size_t>(1, std::min<size_t>(32, (size_t(1) << 30) / (ldu * 8 * kBM)));
+        U.alloc(chunk_tiles * kBM * ldu);
+        StressParams sp{};
+        sp.ldu = static_cast<long long>(ldu);
+        sp.row_cell = row_cell_d.ptr;
+        sp.row_kind = row_kind_d.ptr;
+        sp.row_dt = row_dt_d.ptr;
+        sp.cx = static_cast<int>(m.cells[0]);
+        sp.cy = static_cast<int>(m.cells[1]);
+        sp.cz = static_cast<int>(m.cells[2]);
+        sp.P = points;
+        for (int k = 0; k < 2; ++k) {
+            const RomHost &mk = rom[k].set ? rom[k] : m;
+            sp.hinv[k] = mk.d_hinv.ptr;
+            sp.elem_mat[k] = mk.d_em.ptr;
+            for (int a = 0; a < 3; ++a)
+                for (int b2 = 0; b2 < 3; ++b2) sp.lame[k][a][b2] = mk.lame[a][b2];
+        }
+        sp.out = out;
+        sp.out_cell0 = static_cast<long long>(c0);
+        sp.out_cells = static_cast<long long>(c1 - c0);
+        const size_t smem = 2 * (m.cells[0] + 1) * (m.cells[1] + 1) * 3 * sizeof(double);
+        size_t t = 0;
+        while (t < m_tiles) {
+            if (!need[t]) { ++t; continue; }
+            size_t t1 = t;
+            while (t1 < m_tiles && need[t1] && t1 - t < chunk_tiles && tile_kind[t1] == tile_kind[t]) ++t1;
+            const int kind = tile_kind[t];
+            const RomHost &mk = rom[kind];
+            GemmParams gp{};
+            gp.A = X.ptr + t * kBM * ldk;
+            gp.lda = static_cast<long long>(ldk);
+            gp.Bt[0] = gp.Bt[1] = mk.d_phi.ptr;
+            gp.ldb = static_cast<long long>(ldk);
+            gp.tile_kind = nullptr;
+            gp.C = U.ptr;
+            gp.ldc = static_cast<long long>(ldu);
+            gp.m_tiles = static_cast<int>(t1 - t);
+            gp.n_tiles = static_cast<int>(round_up(mk.n_fine, kBN) / kBN);
+            gp.k_chunks = static_cast<int>(ldk / kKC);
+            gp.n_valid = static_cast<int>(mk.n_fine);
+            gp.n_store = static_cast<int>(mk.n_fine);
+            gp.row_scale = row_dt_d.ptr + t * kBM;
+            gp.col_bias[0] = gp.col_bias[1] = mk.d_ut.ptr;
+            gp.done = nullptr;
+            gp.tile_counter = tile_counter.ptr;
+            gemm_nt_f64<K6Cfg><<<k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
+            sp.U = U.ptr;
+            sp.j0 = static_cast<int>(t * kBM);
+            dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>(m.cells[2]));
+            stress_kernel<<<grid, 256, smem, stream>>>(sp);
+            launches += 2;
+            CK(cudaGetLastError());
+            t = t1;
+        }
+    }
+};
+
+namespace {
+
+template <typename F>
+int guarded(tsv_ctx *ctx, F &&f) {
+    if (!ctx) return TSV_EINVAL;
+    try {
+        int rc = f();
+        if (rc == TSV_OK) ctx->err.clear();
+        return rc;
+    } catch (const StatusError &e) {
+        ctx->err = e.what();
+        return e.code;
+    } catch (const tsvb200::Error &e) {
+        ctx->err = e.what();
+        return TSV_EINVAL;
+    } catch (const std::bad_alloc &) {
+        ctx->err = "host allocation failed";
+        return TSV_ENOMEM;
+    } catch (const std::exception &e) {
+        ctx->err = e.what();
+        return TSV_EINVAL;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tsv_abi_version(void) { return TSV_B200_ABI_VERSION; }
+
+int tsv_index_global_nodes(uint32_t rows, uint32_t cols, const uint32_t q[3], uint64_t *n_dofs, uint32_t lattice[3],
+                           int32_t *nol, uint32_t *lon, uint32_t *dm) {
+    try {
+        if (!q) return TSV_EINVAL;
+        ArrayLayout L;
+        L.rows = rows;
+        L.cols = cols;
+        L.delta_t = {0.0};
+        L.pitch = 1.0;
+        L.height = 1.0;
+        NodeLayout nl = NodeLayout::create(q[0], q[1], q[2]);
+        GlobalIndex idx = index_global_nodes(L, nl);
+        if (n_dofs) *n_dofs = idx.dof_count();
+        if (lattice) {
+            lattice[0] = idx.lat_x;
+            lattice[1] = idx.lat_y;
+            lattice[2] = idx.lat_z;
+        }
+        if (nol) std::memcpy(nol, idx.node_of_lattice.data(), idx.node_of_lattice.size() * sizeof(int32_t));
+        if (lon)
+            for (size_t i = 0; i < idx.node_count(); ++i)
+                for (int c = 0; c < 3; ++c) lon[3 * i + c] = idx.lattice_of_node[i][c];
+        if (dm) {
+            std::vector<uint32_t> m = tsvb200::dof_map(L, idx, nl);
+            std::memcpy(dm, m.data(), m.size() * sizeof(uint32_t));
+        }
+        return TSV_OK;
+    } catch (...) {
+        return TSV_EINVAL;
+    }
+}
+
+int tsv_ctx_create(int device, tsv_ctx **out) {
+    if (!out) return TSV_EINVAL;
+    *out = nullptr;
+    auto ctx = std::make_unique<tsv_ctx>();
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return TSV_ECUDA;
+    int rc = guarded(ctx.get(), [&] {
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&ctx->ev0));
+        CK(cudaEventCreate(&ctx->ev1));
+        CK(cudaMallocHost(&ctx->h_state, sizeof(CgState)));
+        CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaFuncSetAttribute(gemm_nt_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K1Cfg::SMEM)));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_nt_f64<K1Cfg>, K1Cfg::THREADS, K1Cfg::SMEM));
+        ctx->k1_grid = ctx->k6_grid = std::max(1, occ) * ctx->sm_count;
+        ctx->tile_counter.alloc(2);
+        CK(cudaMemset(ctx->tile_counter.ptr, 0, 2 * sizeof(unsigned)));
+        ctx->state.alloc(1);
+        CK(cudaMemset(ctx->state.ptr, 0, sizeof(CgState)));
+        return TSV_OK;
+    });
+    if (rc != TSV_OK) return rc;
+    *out = ctx.release();
+    return TSV_OK;
+}
+
+void tsv_ctx_destroy(tsv_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    delete ctx;
+}
+
+const char *tsv_last_error(const tsv_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
+    return guarded(ctx, [&] {
+        if (kind != 0 && kind != 1) throw StatusError(TSV_EINVAL, "set_rom: kind must be 0 (tsv) or 1 (dummy)");
+        if (!d || !d->a_element || !d->b_element || !d->basis || !d->thermal)
+            throw StatusError(TSV_EINVAL, "set_rom: missing ROM arrays");
+        for (int a = 0; a < 3; ++a) {
+            if (d->q[a] < 2) throw StatusError(TSV_EINVAL, "NodeLayout: need at least 2 interpolation nodes per axis");
+            if (d->grid_len[a] < 2 || !d->grid[a]) throw StatusError(TSV_EINVAL, "grid: axis needs at least 2 lines");
+        }
+        cudaSetDevice(ctx->device);
+        RomHost &m = ctx->rom[kind];
+        m.set = false;
+        std::copy(d->q, d->q + 3, m.q);
+        std::copy(d->geometry, d->geometry + 4, m.geom);
+        for (int a = 0; a < 3; ++a) {
+            m.grid[a].assign(d->grid[a], d->grid[a] + d->grid_len[a]);
+            for (size_t i = 1; i < m.grid[a].size(); ++i)
+                if (!(m.grid[a][i] > m.grid[a][i - 1])) throw StatusError(TSV_EINVAL, "grid: axis must be strictly increasing");
+            m.cells[a] = d->grid_len[a] - 1;
+        }
+        for (int i = 0; i < 3; ++i) {
+            const double E = d->materials[i][0], nu = d->materials[i][1], alpha = d->materials[i][2];
+            if (!(E > 0.0)) throw StatusError(TSV_EINVAL, "material: Young modulus must be > 0");
+            if (!(nu > -1.0) || !(nu < 0.5)) throw StatusError(TSV_EINVAL, "material: Poisson ratio must lie in (-1, 0.5)");
+            // lame_parameters, material.cpp:7-15
+            const double lambda = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+            const double mu = E / (2.0 * (1.0 + nu));
+            m.mats[i][0] = E;
+            m.mats[i][1] = nu;
+            m.mats[i][2] = alpha;
+            m.lame[i][0] = lambda;
+            m.lame[i][1] = mu;
+            m.lame[i][2] = alpha * (3.0 * lambda + 2.0 * mu);
+        }
+        const size_t E = m.cells[0] * m.cells[1] * m.cells[2];
+        m.elem_mat.assign(E, 2);
+        if (d->element_material) {
+            m.elem_mat.assign(d->element_material, d->element_material + E);
+        } else if (kind == 0) {  // classify_tsv by centroid radius, mesh.cpp:182-190
+            const double dd = d->geometry[0], t = d->geometry[2], p = d->geometry[3];
+            for (size_t k = 0; k < m.cells[2]; ++k)
+                for (size_t j = 0; j < m.cells[1]; ++j)
+                    for (size_t i = 0; i < m.cells[0]; ++i) {
+                        const double xc = 0.5 * (m.grid[0][i] + m.grid[0][i + 1]);
+                        const double yc = 0.5 * (m.grid[1][j] + m.grid[1][j + 1]);
+                        const double rr = std::hypot(xc - 0.5 * p, yc - 0.5 * p);
+                        m.elem_mat[(k * m.cells[1] + j) * m.cells[0] + i] =
+                            rr < 0.5 * dd ? 0 : (rr < 0.5 * dd + t ? 1 : 2);
+                    }
+        }
+        for (uint8_t v : m.elem_mat)
+            if (v > 2) throw StatusError(TSV_EINVAL, "set_rom: element material id out of range");
+        const size_t n = num_element_dofs(d->q[0], d->q[1], d->q[2]);
+        const size_t n_fine = (m.cells[0] + 1) * (m.cells[1] + 1) * (m.cells[2] + 1) * 3;
+        m.n = n;
+        m.n_fine = n_fine;
+        std::memcpy(m.fingerprint, d->fingerprint, 32);
+        m.k_r.assign(d->a_element, d->a_element + n * n);
+        m.b_el.assign(d->b_element, d->b_element + n);
+        m.u_t.assign(d->thermal, d->thermal + n_fine);
+        const size_t ldk = round_up(n, kKC);
+        {
+            std::vector<double> kp(round_up(n, kBN) * ldk, 0.0);
+            for (size_t a = 0; a < n; ++a)
+                for (size_t k = 0; k < n; ++k) kp[a * ldk + k] = d->a_element[a * n + k];
+            m.d_k.upload(kp.data(), kp.size(), ctx->stream);
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        {
+            const size_t rows = round_up(n_fine, kBN);
+            std::vector<double> pp(rows * ldk, 0.0);
+            for (size_t f = 0; f < n_fine; ++f) std::memcpy(pp.data() + f * ldk, d->basis + f * n, n * sizeof(double));
+            m.d_phi.upload(pp.data(), pp.size(), ctx->stream);
+            std::vector<double> ut(rows, 0.0);
+            std::memcpy(ut.data(), d->thermal, n_fine * sizeof(double));
+            m.d_ut.upload(ut.data(), ut.size(), ctx->stream);
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        std::vector<double> hinv;
+        for (int a = 0; a < 3; ++a)
+            for (size_t i = 0; i < m.cells[a]; ++i) hinv.push_back(1.0 / (m.grid[a][i + 1] - m.grid[a][i]));
+        m.d_hinv.upload(hinv.data(), hinv.size(), ctx->stream);
+        m.d_em.upload(m.elem_mat.data(), E, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+        m.set = true;
+        ctx->layout_set = false;  // layout tables depend on the RomSet
+        ctx->drop_graph();
+        ctx->solution_valid = false;
+        return TSV_OK;
+    });
+}
+
+int tsv_set_layout(tsv_ctx *ctx, uint32_t rows, uint32_t cols, const uint8_t *kinds, const double *delta_t,
+                   size_t n_delta_t, double pitch, double height) {
+    return guarded(ctx, [&] {
+        cudaSetDevice(ctx->device);
+        ctx->build_layout(rows, cols, kinds, delta_t, n_delta_t, pitch, height);
+        return TSV_OK;
+    });
+}
+
+int tsv_set_dirichlet(tsv_ctx *ctx, size_t count, const uint32_t *dofs, const double *values) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "set_dirichlet: no layout set");
+        if (count && (!dofs || !values)) throw StatusError(TSV_EINVAL, "set_dirichlet: NULL arrays");
+        DirichletSet set;
+        for (size_t i = 0; i < count; ++i) set.set(dofs[i], values[i]);
+        std::vector<uint8_t> mask(ctx->N, 0);
+        std::vector<double> vals(ctx->N, 0.0);
+        for (const auto &e : set.entries()) {
+            if (e.first >= ctx->N)
+                throw StatusError(TSV_EINVAL, "apply_dirichlet_lifting: dof " + std::to_string(e.first) + " out of range");
+            mask[e.first] = 1;
+            vals[e.first] = e.second;
+        }
+        cudaSetDevice(ctx->device);
+        ctx->drop_graph();
+        ctx->set_bc_mask(std::move(mask), std::move(vals));
+        return TSV_OK;
+    });
+}
+
+int tsv_set_bc(tsv_ctx *ctx, int bc_kind) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "set_bc: no layout set");
+        if (bc_kind < 0 || bc_kind > 3) throw StatusError(TSV_EINVAL, "set_bc: unknown boundary condition");
+        DirichletSet set = reduced_dirichlet(static_cast<BcKind>(bc_kind), ctx->index);
+        std::vector<uint8_t> mask(ctx->N, 0);
+        std::vector<double> vals(ctx->N, 0.0);
+        for (const auto &e : set.entries()) {
+            mask[e.first] = 1;
+            vals[e.first] = e.second;
+        }
+        cudaSetDevice(ctx->device);
+        ctx->drop_graph();
+        ctx->set_bc_mask(std::move(mask), std::move(vals));
+        return TSV_OK;
+    });
+}
+
+int tsv_get_index(tsv_ctx *ctx, uint64_t *n_dofs, uint64_t *n_nodes, uint32_t lattice[3], uint32_t *n_reduced) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_index: no layout set");
+        if (n_dofs) *n_dofs = ctx->N;
+        if (n_nodes) *n_nodes = ctx->nodes;
+        if (lattice) {
+            lattice[0] = ctx->index.lat_x;
+            lattice[1] = ctx->index.lat_y;
+            lattice[2] = ctx->index.lat_z;
+        }
+        if (n_reduced) *n_reduced = static_cast<uint32_t>(ctx->n);
+        return TSV_OK;
+    });
+}
+
+int tsv_get_dof_map(tsv_ctx *ctx, uint32_t *out) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_dof_map: no layout set");
+        std::memcpy(out, ctx->dofmap.data(), ctx->dofmap.size() * sizeof(uint32_t));
+        return TSV_OK;
+    });
+}
+
+int tsv_get_lattice(tsv_ctx *ctx, int32_t *nol, uint32_t *lon) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_lattice: no layout set");
+        if (nol) std::memcpy(nol, ctx->index.node_of_lattice.data(), ctx->index.node_of_lattice.size() * 4);
+        if (lon)
+            for (size_t i = 0; i < ctx->nodes; ++i)
+                for (int c = 0; c < 3; ++c) lon[3 * i + c] = ctx->index.lattice_of_node[i][c];
+        return TSV_OK;
+    });
+}
+
+int tsv_get_constrained(tsv_ctx *ctx, uint8_t *mask) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_constrained: no layout set");
+        std::memcpy(mask, ctx->constrained.data(), ctx->N);
+        return TSV_OK;
+    });
+}
+
+int tsv_get_load(tsv_ctx *ctx, double *bout) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_load: no layout set");
+        cudaSetDevice(ctx->device);
+        std::vector<double> bi(ctx->N);
+        CK(cudaMemcpy(bi.data(), ctx->b.ptr, ctx->N * sizeof(double), cudaMemcpyDeviceToHost));
+        ctx->to_reference(bi.data(), bout);
+        return TSV_OK;
+    });
+}
+
+int tsv_apply(tsv_ctx *ctx, const double *xin, double *yout) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "apply: no layout set");
+        cudaSetDevice(ctx->device);
+        std::vector<double> xi = ctx->to_internal(xin);
+        ctx->r.upload(xi.data(), ctx->N, ctx->stream);
+        ctx->launch_scatter(ctx->r.ptr, 0);
+        ctx->launch_k1(nullptr);
+        gather_vec_kernel<<<ctx->vec_grid(), kVecThreads, 0, ctx->stream>>>(
+            static_cast<int>(ctx->nodes), ctx->slots.ptr, ctx->cmask.ptr, ctx->Y.ptr, ctx->r.ptr, ctx->ap.ptr, 0);
+        ++ctx->launches;
+        CK(cudaGetLastError());
+        std::vector<double> yi(ctx->N);
+        CK(cudaMemcpyAsync(yi.data(), ctx->ap.ptr, ctx->N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->to_reference(yi.data(), yout);
+        return TSV_OK;
+    });
+}
+
+int tsv_solve(tsv_ctx *ctx, const tsv_iter_options *opts, double *u_out, tsv_solve_info *info) {
+    return guarded(ctx, [&] {
+        if (!opts) throw StatusError(TSV_EINVAL, "solve: NULL options");
+        cudaSetDevice(ctx->device);
+        return ctx->solve(*opts, u_out, info);
+    });
+}
+
+int tsv_set_solution(tsv_ctx *ctx, const double *u) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "set_solution: no layout set");
+        cudaSetDevice(ctx->device);
+        std::vector<double> ui = ctx->to_internal(u);
+        ctx->x.upload(ui.data(), ctx->N, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->solution_valid = true;
+        return TSV_OK;
+    });
+}
+
+int tsv_recover(tsv_ctx *ctx, int points, uint64_t c0, uint64_t c1, double *out) {
+    return guarded(ctx, [&] {
+        cudaSetDevice(ctx->device);
+        ctx->check_recovery(points);
+        if (c0 > c1 || c1 > ctx->B) throw StatusError(TSV_EINVAL, "recover: cell range out of bounds");
+        if (c0 == c1) return TSV_OK;
+        const size_t per_cell = ctx->elems() * static_cast<size_t>(points) * 7;
+        const size_t max_cells = std::max<size_t>(1, (size_t(2) << 30) / (per_cell * sizeof(double)));
+        DevBuf<double> dout;
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        for (size_t a = c0; a < c1; a += max_cells) {
+            const size_t b2 = std::min<size_t>(c1, a + max_cells);
+            dout.alloc((b2 - a) * per_cell);
+            ctx->recover_range(points, a, b2, dout.ptr);
+            CK(cudaMemcpyAsync(out + (a - c0) * per_cell, dout.ptr, (b2 - a) * per_cell * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->last_recover_ms = ms;
+        return TSV_OK;
+    });
+}
+
+int tsv_recover_resident(tsv_ctx *ctx, int points) {
+    return guarded(ctx, [&] {
+        cudaSetDevice(ctx->device);
+        ctx->check_recovery(points);
+        const size_t per_cell = ctx->elems() * static_cast<size_t>(points) * 7;
+        ctx->stress.alloc(ctx->B * per_cell);
+        ctx->stress_points = points;
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        ctx->recover_range(points, 0, ctx->B, ctx->stress.ptr);
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->last_recover_ms = ms;
+        return TSV_OK;
+    });
+}
+
+int tsv_copy_stress(tsv_ctx *ctx, uint64_t c0, uint64_t c1, double *out) {
+    return guarded(ctx, [&] {
+        if (!ctx->stress.ptr) throw StatusError(TSV_ESTATE, "copy_stress: call tsv_recover_resident first");
+        if (c0 > c1 || c1 > ctx->B) throw StatusError(TSV_EINVAL, "copy_stress: cell range out of bounds");
+        cudaSetDevice(ctx->device);
+        const size_t per_cell = ctx->elems() * static_cast<size_t>(ctx->stress_points) * 7;
+        CK(cudaMemcpy(out, ctx->stress.ptr + c0 * per_cell, (c1 - c0) * per_cell * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+        return TSV_OK;
+    });
+}
+
+int tsv_block_field(tsv_ctx *ctx, uint64_t cell, double *out) {
+    return guarded(ctx, [&] {
+        cudaSetDevice(ctx->device);
+        ctx->check_recovery(8);
+        if (cell >= ctx->B) throw StatusError(TSV_EINVAL, "block_field: cell out of range");
+        const int j = ctx->cell_row[cell];
+        const size_t t = j / kBM;
+        const RomHost &mk = ctx->rom[ctx->tile_kind[t]];
+        const size_t ldu = round_up(mk.n_fine, 8);
+        ctx->launch_scatter(ctx->x.ptr, 1);
+        ctx->U.alloc(std::max(ctx->U.count, kBM * ldu));
+        GemmParams gp{};
+        gp.A = ctx->X.ptr + t * kBM * ctx->ldk;
+        gp.lda = static_cast<long long>(ctx->ldk);
+        gp.Bt[0] = gp.Bt[1] = mk.d_phi.ptr;
+        gp.ldb = static_cast<long long>(ctx->ldk);
+        gp.C = ctx->U.ptr;
+        gp.ldc = static_cast<long long>(ldu);
+        gp.m_tiles = 1;
+        gp.n_tiles = static_cast<int>(round_up(mk.n_fine, kBN) / kBN);
+        gp.k_chunks = static_cast<int>(ctx->ldk / kKC);
+        gp.n_valid = gp.n_store = static_cast<int>(mk.n_fine);
+        gp.row_scale = ctx->row_dt_d.ptr + t * kBM;
+        gp.col_bias[0] = gp.col_bias[1] = mk.d_ut.ptr;
+        gp.tile_counter = ctx->tile_counter.ptr;
+        gemm_nt_f64<K6Cfg><<<ctx->k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, ctx->stream>>>(gp);
+        ++ctx->launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, ctx->U.ptr + (j - t * kBM) * ldu, mk.n_fine * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return TSV_OK;
+    });
+}
+
+int tsv_profile_apply(tsv_ctx *ctx, int reps, double *ms_per_launch) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "profile_apply: no layout set");
+        if (reps < 1) throw StatusError(TSV_EINVAL, "profile_apply: reps must be >= 1");
+        cudaSetDevice(ctx->device);
+        ctx->launch_k1(nullptr);  // warm-up
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        for (int i = 0; i < reps; ++i) ctx->launch_k1(nullptr);
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->last_apply_ms = ms / reps;
+        if (ms_per_launch) *ms_per_launch = ctx->last_apply_ms;
+        return TSV_OK;
+    });
+}
+
+int tsv_get_timing(tsv_ctx *ctx, tsv_timing *out) {
+    return guarded(ctx, [&] {
+        out->solve_ms = ctx->last_solve_ms;
+        out->recover_ms = ctx->last_recover_ms;
+        out->apply_ms_avg = ctx->last_apply_ms;
+        out->kernel_launches = ctx->launches;
+        return TSV_OK;
+    });
+}
+
+}  // extern "C"

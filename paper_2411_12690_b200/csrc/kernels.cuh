@@ -1,0 +1,610 @@
+// sm_100a kernels of the online stage.
+//
+//   gemm_nt_f64      K1 operator apply  Y = X K_r        (blocks x n x n, DMMA)
+//                    K6 block recovery  U = Q Phi^T + dT u_T^T (blocks x n_fine x n)
+//   cg_gather_*      K1 scatter half + K2/K5: owner-computes sum of the
+//                    per-block products, PCG vector updates, fused dots
+//   cg_scatter_*     K1 gather half: write the next operand into the
+//                    block-major X panel (one slot per (block, local DoF))
+//   stress_gauss     K7 Gauss-point / centroid stress + von Mises
+//
+// FP64 tensor-core work on sm_100a is warp-level mma.sync m8n8k4 (SASS
+// DMMA.8x8x4); tcgen05 has no kind::f64.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsvb200 {
+
+// ------------------------------------------------------------------ GEMM
+// C[m][n] = sum_k A[m][k] * Bt[n][k]  (+ row_scale[m] * col_bias[n]).
+// A: block-major operand panel, rows = blocks (GEMM row order), k contiguous.
+// Bt: K_r (symmetric, so K_r^T = K_r) or Phi (row-major [fine dof][k]).
+struct GemmParams {
+    const double *A;
+    long long lda;
+    const double *Bt[2];  // per block kind
+    long long ldb;
+    const uint8_t *tile_kind;  // per M tile
+    double *C;
+    long long ldc;
+    int m_tiles, n_tiles, k_chunks;
+    int n_valid;  // columns with data; fragments beyond are skipped
+    int n_store;  // columns written
+    const double *row_scale;     // nullable: dT per row (K6 epilogue)
+    const double *col_bias[2];   // u_T per kind
+    const int *done;             // nullable: early exit when *done != 0
+    unsigned *tile_counter;      // [2] {next tile, exited CTAs}, zero between launches
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int BM_, int BN_, int WM_, int WN_, int KC_, int STAGES_>
+struct GemmCfg {
+    static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, KC = KC_, STAGES = STAGES_;
+    static constexpr int THREADS = WM * WN * 32;
+    static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
+    // Row pitch KC+4 doubles: 8-byte fragment loads of a half-warp (4 rows x
+    // 4 k) hit 16 distinct 8-byte bank pairs (pitch mod 16 == 4).
+    static constexpr int SP = KC + 4;
+    static constexpr int A_STAGE = BM * SP, B_STAGE = BN * SP;
+    static constexpr size_t SMEM = size_t(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
+    static_assert(TM % 8 == 0 && TN % 8 == 0 && KC % 4 == 0, "tile shape");
+};
+
+template <class Cfg>
+__device__ __forceinline__ void gemm_load_stage(double *As, double *Bs, const double *A0, long long lda,
+                                                const double *B0, long long ldb, int kc) {
+    constexpr int CPR = Cfg::KC / 2;  // 16-byte chunks per row
+    const int tid = threadIdx.x;
+    const long long k0 = static_cast<long long>(kc) * Cfg::KC;
+#pragma unroll
+    for (int i = tid; i < Cfg::BM * CPR; i += Cfg::THREADS) {
+        const int r = i / CPR, c = i % CPR;
+        cp_async16(As + r * Cfg::SP + 2 * c, A0 + r * lda + k0 + 2 * c);
+    }
+#pragma unroll
+    for (int i = tid; i < Cfg::BN * CPR; i += Cfg::THREADS) {
+        const int r = i / CPR, c = i % CPR;
+        cp_async16(Bs + r * Cfg::SP + 2 * c, B0 + r * ldb + k0 + 2 * c);
+    }
+}
+
+// Persistent DMMA GEMM: grid = resident CTAs, tiles handed out by an atomic
+// counter (M tile major, N tile minor, so concurrently running CTAs share
+// the streamed A panel in L2).
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 2) gemm_nt_f64(GemmParams p) {
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_tile;
+    double *As = smem;
+    double *Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+    const int total = p.m_tiles * p.n_tiles;
+    const int nf_valid = (p.n_valid + 7) / 8;
+    const bool skip = p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0;
+
+    while (!skip) {
+        if (tid == 0) s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
+        __syncthreads();
+        const int tile = s_tile;
+        __syncthreads();
+        if (tile >= total) break;
+        const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
+        const double *A0 = p.A + static_cast<long long>(mt) * Cfg::BM * p.lda;
+        const double *B0 = (kind ? p.Bt[1] : p.Bt[0]) + static_cast<long long>(nt) * Cfg::BN * p.ldb;
+        const int frag0 = nt * (Cfg::BN / 8) + wn * Cfg::FN;
+        const int fn_lim = min(Cfg::FN, max(0, nf_valid - frag0));
+
+        double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+        for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+            if (s < p.k_chunks)
+                gemm_load_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, s);
+            cp_async_commit();
+        }
+        for (int kc = 0; kc < p.k_chunks; ++kc) {
+            cp_async_wait<Cfg::STAGES - 2>();
+            __syncthreads();
+            const int nk = kc + Cfg::STAGES - 1;
+            if (nk < p.k_chunks) {
+                const int st = nk % Cfg::STAGES;
+                gemm_load_stage<Cfg>(As + st * Cfg::A_STAGE, Bs + st * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, nk);
+            }
+            cp_async_commit();
+            const double *as = As + (kc % Cfg::STAGES) * Cfg::A_STAGE + (wm * Cfg::TM + (lane >> 2)) * Cfg::SP + (lane & 3);
+            const double *bs = Bs + (kc % Cfg::STAGES) * Cfg::B_STAGE + (wn * Cfg::TN + (lane >> 2)) * Cfg::SP + (lane & 3);
+#pragma unroll
+            for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
+                double af[Cfg::FM], bf[Cfg::FN];
+#pragma unroll
+                for (int i = 0; i < Cfg::FM; ++i) af[i] = as[i * 8 * Cfg::SP + ks * 4];
+#pragma unroll
+                for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[j * 8 * Cfg::SP + ks * 4];
+#pragma unroll
+                for (int j = 0; j < Cfg::FN; ++j) {
+                    if (j < fn_lim) {
+#pragma unroll
+                        for (int i = 0; i < Cfg::FM; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                    }
+                }
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+
+        // Epilogue: lane holds C[row][col], C[row][col+1].
+        const long long row0 = static_cast<long long>(mt) * Cfg::BM + wm * Cfg::TM + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+            const int col = nt * Cfg::BN + wn * Cfg::TN + j * 8 + 2 * (lane & 3);
+            if (col >= p.n_store) continue;
+            double b0 = 0.0, b1 = 0.0;
+            const double *cb = kind ? p.col_bias[1] : p.col_bias[0];
+            if (p.row_scale) {
+                b0 = cb[col];
+                b1 = col + 1 < p.n_store ? cb[col + 1] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < Cfg::FM; ++i) {
+                const long long row = row0 + i * 8;
+                double v0 = acc[i][j][0], v1 = acc[i][j][1];
+                if (p.row_scale) {
+                    const double s = p.row_scale[row];
+                    v0 += s * b0;
+                    v1 += s * b1;
+                }
+                double *dst = p.C + row * p.ldc + col;
+                if (col + 1 < p.n_store) {
+                    *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
+                } else {
+                    dst[0] = v0;
+                }
+            }
+        }
+    }
+    // The last CTA out resets the tile counter for the next launch.
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&p.tile_counter[1], 1u) == gridDim.x - 1) {
+            p.tile_counter[0] = 0u;
+            p.tile_counter[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+// ------------------------------------------------------------------- CG
+// Iteration state on the device (cg_solve control flow, linalg.cpp:292-362).
+enum : int { CG_RUNNING = 0, CG_CONVERGED = 1, CG_NOCONV = 2, CG_BREAKDOWN = 3 };
+enum : int { PH_INIT = 0, PH_NORMAL = 1, PH_RESTART = 2 };
+
+struct CgState {
+    int done;       // CG_*
+    int y_holds_x;  // 1: the next product is A x (true-residual verification)
+    int phase;      // what the B kernel does this iteration
+    int p_assign;   // 1: p = z (fresh start), 0: p = z + beta p
+    int it, best_it, max_it, breakdown_code;
+    double rho, alpha, beta, res, best_res, norm_b, tol, tol_abs;
+    unsigned ticket_a, ticket_b;
+};
+
+struct CgParams {
+    CgState *st;
+    int n_nodes;
+    const int *slots;   // [node][4] offsets into X / Y (-1 = none), ascending block order
+    const uint8_t *cmask;  // [dof] constrained
+    const double *b;
+    double *x, *r, *p, *ap;
+    const double *Y;    // block products
+    double *X;          // block-major operand panel
+    int precond;        // 0 none, 1 diagonal, 2 3x3 node blocks
+    const double *pre;  // inv_diag [dof] or inverse node blocks [node][9]
+    double *partial;    // [grid][2]
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block reduction of up to two values (fixed tree order).
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *sh /* [32*NV] */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) sh[warp * NV + i] = v[i];
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            double t = lane < nw ? sh[lane * NV + i] : 0.0;
+            v[i] = warp_sum(t);
+        }
+    }
+}
+
+// Sum of per-CTA partials in CTA order by one warp (the last CTA of a grid).
+template <int NV>
+__device__ __forceinline__ void grid_sum(const double *partial, int nblocks, double (&out)[NV]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = 0.0;
+        for (int k = lane; k < nblocks; k += 32) s += partial[k * NV + i];
+        out[i] = warp_sum(s);
+    }
+}
+
+__device__ __forceinline__ void precond_node(int kind, const double *pre, int node, const double r[3], double z[3]) {
+    if (kind == 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) z[c] = pre[3 * node + c] * r[c];
+    } else if (kind == 2) {
+        const double *m = pre + 9 * static_cast<long long>(node);
+        z[0] = m[0] * r[0] + m[1] * r[1] + m[2] * r[2];
+        z[1] = m[3] * r[0] + m[4] * r[1] + m[5] * r[2];
+        z[2] = m[6] * r[0] + m[7] * r[1] + m[8] * r[2];
+    } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) z[c] = r[c];
+    }
+}
+
+// A: Y (= A p or A x) summed per owned DoF; p'Ap or the true residual.
+__global__ void cg_gather_kernel(CgParams q) {
+    __shared__ double sh[64];
+    __shared__ bool last;
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int yx = st->y_holds_x;
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    double part[1] = {0.0};
+    if (node < q.n_nodes) {
+        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = 3LL * node + c;
+            double acc;
+            if (q.cmask[dof]) {
+                acc = yx ? q.x[dof] : q.p[dof];  // unit row of the lifted matrix
+            } else {
+                acc = 0.0;
+                if (s.x >= 0) acc += q.Y[s.x + c];
+                if (s.y >= 0) acc += q.Y[s.y + c];
+                if (s.z >= 0) acc += q.Y[s.z + c];
+                if (s.w >= 0) acc += q.Y[s.w + c];
+            }
+            if (!yx) {
+                q.ap[dof] = acc;
+                part[0] += q.p[dof] * acc;
+            } else {
+                const double rt = q.b[dof] - acc;
+                q.r[dof] = rt;
+                part[0] += rt * rt;
+            }
+        }
+    }
+    block_sum<1>(part, sh);
+    if (threadIdx.x == 0) {
+        q.partial[blockIdx.x] = part[0];
+        __threadfence();
+        last = atomicAdd(&st->ticket_a, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    __threadfence();
+    double tot[1];
+    grid_sum<1>(q.partial, gridDim.x, tot);
+    if (threadIdx.x == 0) {
+        st->ticket_a = 0u;
+        if (!yx) {
+            const double pap = tot[0];
+            if (!isfinite(pap)) {
+                st->done = CG_BREAKDOWN;
+                st->breakdown_code = 1;  // NaN/Inf
+            } else if (pap <= 0.0) {
+                st->done = CG_BREAKDOWN;
+                st->breakdown_code = 2;  // p'Ap <= 0
+            } else {
+                st->alpha = st->rho / pap;
+            }
+            st->phase = PH_NORMAL;
+        } else {
+            st->res = sqrt(tot[0]);
+            if (st->res <= st->tol_abs) st->done = CG_CONVERGED;
+            st->phase = PH_RESTART;
+        }
+        __threadfence();
+    }
+}
+
+// B: x += alpha p, r -= alpha Ap, z = M r, (r.z, r.r); or the restart /
+// initial variants. The last CTA advances the iteration counter and
+// decides what the next operator product is (loop head of cg_solve).
+__global__ void cg_update_kernel(CgParams q) {
+    __shared__ double sh[64];
+    __shared__ bool last;
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int phase = st->phase;
+    const double alpha = st->alpha;
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    double part[2] = {0.0, 0.0};
+    if (node < q.n_nodes) {
+        double r3[3], z3[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = 3LL * node + c;
+            double rv;
+            if (phase == PH_NORMAL) {
+                q.x[dof] += alpha * q.p[dof];
+                rv = q.r[dof] - alpha * q.ap[dof];
+                q.r[dof] = rv;
+            } else if (phase == PH_INIT) {
+                q.x[dof] = 0.0;
+                rv = q.b[dof];  // r = b - A*0
+                q.r[dof] = rv;
+            } else {
+                rv = q.r[dof];
+            }
+            r3[c] = rv;
+        }
+        precond_node(q.precond, q.pre, node, r3, z3);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            part[0] += r3[c] * z3[c];
+            part[1] += r3[c] * r3[c];
+        }
+    }
+    block_sum<2>(part, sh);
+    if (threadIdx.x == 0) {
+        q.partial[2 * blockIdx.x] = part[0];
+        q.partial[2 * blockIdx.x + 1] = part[1];
+        __threadfence();
+        last = atomicAdd(&st->ticket_b, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x >= 32) return;
+    __threadfence();
+    double tot[2];
+    grid_sum<2>(q.partial, gridDim.x, tot);
+    if (threadIdx.x != 0) return;
+    st->ticket_b = 0u;
+    if (phase == PH_INIT) {
+        st->norm_b = sqrt(tot[1]);
+        st->tol_abs = st->tol * st->norm_b;
+        st->rho = tot[0];
+        st->res = st->norm_b;
+        st->best_res = st->res;
+        st->best_it = 0;
+        st->it = 0;
+        st->p_assign = 1;
+        if (!isfinite(st->norm_b)) {
+            st->done = CG_BREAKDOWN;
+            st->breakdown_code = 1;
+        } else if (st->norm_b == 0.0) {
+            st->done = CG_CONVERGED;  // x = 0 solves exactly (linalg.cpp:298)
+        } else {
+            st->y_holds_x = st->res <= st->tol_abs ? 1 : 0;
+        }
+    } else if (phase == PH_RESTART) {
+        st->rho = tot[0];
+        st->p_assign = 1;
+        st->y_holds_x = 0;
+    } else {
+        const double rho_next = tot[0];
+        st->beta = rho_next / st->rho;
+        st->rho = rho_next;
+        st->res = sqrt(tot[1]);
+        st->p_assign = 0;
+        if (!isfinite(st->res)) {
+            st->done = CG_BREAKDOWN;
+            st->breakdown_code = 1;
+        } else {
+            st->it += 1;
+            if (st->res < st->best_res) {
+                st->best_res = st->res;
+                st->best_it = st->it;
+            }
+            if (st->it >= st->max_it) {
+                st->done = (st->res / st->norm_b <= st->tol) ? CG_CONVERGED : CG_NOCONV;
+            } else {
+                st->y_holds_x = st->res <= st->tol_abs ? 1 : 0;
+            }
+        }
+    }
+    __threadfence();
+}
+
+// C: p = z + beta p (or p = z), then write the next operator operand (p,
+// or x for a verification) into the block-major panel, free DoFs only.
+__global__ void cg_scatter_kernel(CgParams q) {
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= q.n_nodes) return;
+    const int p_assign = st->p_assign, yx = st->y_holds_x;
+    const double beta = st->beta;
+    double r3[3], z3[3], v[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) r3[c] = q.r[3LL * node + c];
+    precond_node(q.precond, q.pre, node, r3, z3);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const long long dof = 3LL * node + c;
+        const double pn = p_assign ? z3[c] : z3[c] + beta * q.p[dof];
+        q.p[dof] = pn;
+        v[c] = yx ? q.x[dof] : pn;
+    }
+    const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+    const int sl[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (q.cmask[3LL * node + c]) continue;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (sl[k] >= 0) q.X[sl[k] + c] = v[c];
+    }
+}
+
+// Plain gather/scatter helpers (tsv_apply, recovery, RHS lifting).
+// mode 0: X[slot] = v (free DoFs only, constrained slots zeroed)
+// mode 1: X[slot] = v for every DoF (recovery uses u at all DoFs)
+// mode 2: X[slot] = v on constrained DoFs only, 0 elsewhere (A_fc g)
+__global__ void scatter_vec_kernel(int n_nodes, const int *slots, const uint8_t *cmask, const double *v,
+                                   double *X, int mode) {
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= n_nodes) return;
+    const int4 s = reinterpret_cast<const int4 *>(slots)[node];
+    const int sl[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const long long dof = 3LL * node + c;
+        const bool cm = cmask[dof] != 0;
+        double val = v[dof];
+        if ((mode == 0 && cm) || (mode == 2 && !cm)) val = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (sl[k] >= 0) X[sl[k] + c] = val;
+    }
+}
+
+// y = Mf o sum(Y) + Mc o x  (mode 0), or b_f -= sum(Y), b_c = g (mode 1).
+__global__ void gather_vec_kernel(int n_nodes, const int *slots, const uint8_t *cmask, const double *Y,
+                                  const double *x, double *y, int mode) {
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= n_nodes) return;
+    const int4 s = reinterpret_cast<const int4 *>(slots)[node];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const long long dof = 3LL * node + c;
+        double acc = 0.0;
+        if (s.x >= 0) acc += Y[s.x + c];
+        if (s.y >= 0) acc += Y[s.y + c];
+        if (s.z >= 0) acc += Y[s.z + c];
+        if (s.w >= 0) acc += Y[s.w + c];
+        if (mode == 0) {
+            y[dof] = cmask[dof] ? x[dof] : acc;
+        } else {
+            y[dof] = cmask[dof] ? x[dof] : y[dof] - acc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- stress
+// K7: strain/stress/von Mises at Gauss points (or centroids) of every
+// element of a chunk of blocks, from the reconstructed fine field U.
+struct StressParams {
+    const double *U;
+    long long ldu;
+    int j0;               // first GEMM row of the chunk
+    const int *row_cell;  // GEMM row -> original cell (-1 = padding)
+    const uint8_t *row_kind;
+    const double *row_dt;
+    int cx, cy, cz, P;
+    const double *hinv[2];    // [kind][cx + cy + cz]: 1/h per axis cell (x, then y, then z)
+    const uint8_t *elem_mat[2];
+    double lame[2][3][3];     // [kind][mat] lambda, mu, alpha*(3 lambda + 2 mu)
+    double *out;
+    long long out_cell0;      // first original cell of the output range
+    long long out_cells;      // cells in the output range
+};
+
+__global__ void stress_kernel(StressParams sp) {
+    extern __shared__ double su[];  // two node layers: 2 * nxy * 3
+    const int jr = blockIdx.x;       // row within chunk
+    const int k = blockIdx.y;        // element layer
+    const int j = sp.j0 + jr;
+    const int cell = sp.row_cell[j];
+    if (cell < 0) return;
+    const long long oc = cell - sp.out_cell0;
+    if (oc < 0 || oc >= sp.out_cells) return;
+    const int kind = sp.row_kind[j];
+    const int nx = sp.cx + 1, ny = sp.cy + 1, nxy = nx * ny;
+    const double *U = sp.U + static_cast<long long>(jr) * sp.ldu + static_cast<long long>(k) * nxy * 3;
+    for (int i = threadIdx.x; i < 2 * nxy * 3; i += blockDim.x) su[i] = U[i];
+    __syncthreads();
+    const double dt = sp.row_dt[j];
+    const double *hx = sp.hinv[kind], *hy = hx + sp.cx, *hz = hy + sp.cy;
+    const double hzi = hz[k];
+    const int P = sp.P;
+    const int per_layer = sp.cx * sp.cy * P;
+    const long long E = static_cast<long long>(sp.cx) * sp.cy * sp.cz;
+    const double g = 0.57735026918962576451;  // 1/sqrt(3)
+    double *out_cell = sp.out + oc * E * P * 7;
+    for (int t = threadIdx.x; t < per_layer; t += blockDim.x) {
+        const int gp = t % P, e2 = t / P;
+        const int i = e2 % sp.cx, jj = e2 / sp.cx;
+        const long long e = (static_cast<long long>(k) * sp.cy + jj) * sp.cx + i;
+        double xi = 0.0, eta = 0.0, zeta = 0.0;
+        if (P == 8) {
+            xi = (gp >> 2) ? g : -g;
+            eta = ((gp >> 1) & 1) ? g : -g;
+            zeta = (gp & 1) ? g : -g;
+        }
+        const double hxi = hx[i], hyi = hy[jj];
+        double du[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int di = (a == 1 || a == 2 || a == 5 || a == 6);
+            const int dj = (a == 2 || a == 3 || a == 6 || a == 7);
+            const int dk = a >= 4;
+            const double sx = di ? 1.0 : -1.0, sy = dj ? 1.0 : -1.0, sz = dk ? 1.0 : -1.0;
+            // grad N_a = J^-1 dN/dxi with J = diag(h/2) for box cells (fem.cpp:27-58)
+            const double gxa = 0.25 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta) * hxi;
+            const double gya = 0.25 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta) * hyi;
+            const double gza = 0.25 * sz * (1.0 + sx * xi) * (1.0 + sy * eta) * hzi;
+            const double *ua = su + (dk * nxy + (jj + dj) * nx + (i + di)) * 3;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                du[c][0] += ua[c] * gxa;
+                du[c][1] += ua[c] * gya;
+                du[c][2] += ua[c] * gza;
+            }
+        }
+        const int mat = sp.elem_mat[kind][e];
+        const double lambda = sp.lame[kind][mat][0], mu = sp.lame[kind][mat][1];
+        const double thermal = sp.lame[kind][mat][2] * dt;
+        const double exx = du[0][0], eyy = du[1][1], ezz = du[2][2];
+        const double exy = 0.5 * (du[0][1] + du[1][0]);
+        const double eyz = 0.5 * (du[1][2] + du[2][1]);
+        const double ezx = 0.5 * (du[2][0] + du[0][2]);
+        const double tr = exx + eyy + ezz;
+        const double sxx = lambda * tr + 2.0 * mu * exx - thermal;
+        const double syy = lambda * tr + 2.0 * mu * eyy - thermal;
+        const double szz = lambda * tr + 2.0 * mu * ezz - thermal;
+        const double sxy = 2.0 * mu * exy, syz = 2.0 * mu * eyz, szx = 2.0 * mu * ezx;
+        const double d1 = sxx - syy, d2 = syy - szz, d3 = szz - sxx;
+        const double vm2 = 0.5 * (d1 * d1 + d2 * d2 + d3 * d3) + 3.0 * (sxy * sxy + syz * syz + szx * szx);
+        double *o = out_cell + (e * P + gp) * 7;
+        o[0] = sxx; o[1] = syy; o[2] = szz; o[3] = sxy; o[4] = syz; o[5] = szx;
+        o[6] = sqrt(fmax(vm2, 0.0));
+    }
+}
+
+}  // namespace tsvb200
