@@ -1,0 +1,384 @@
+#!/usr/bin/env python3
+"""Online-stage benchmark: TSV blocks/s of (reduced solve + stress recovery).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One step = one pass of the hot path over the whole array: the reduced
+global solve (matrix-free FP64 Jacobi-PCG from x0 = 0 to relative residual
+1e-12, reference control flow linalg.cpp:292-362) followed by 2x2x2
+Gauss-point (or centroid) stress + von Mises recovery of every block.
+
+  value  blocks/s with ROMs/layout resident in HBM, device time (CUDA events
+         on the context stream) of K steps, max over ranks, summed over ranks
+         (replicas: weak scaling)
+  e2e    the same through the public C ABI with host buffers every step:
+         layout + dT upload (index/lifting on the host), solve with the
+         solution read back, and the full stress field read back into pinned
+         host memory
+The ROM (local stage) is built once on the GPU by the product's own
+tsv_build_rom and timed separately. --impl reference times the reference's
+own CPU implementation (oracle/_ref: the unmodified tsvstress sources) on
+the host cores for the same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TSV blocks/s (reduced solve + stress recovery); % of FP64/HBM roofline"
+TOL = 1e-12
+BC = "bottom_pin_321"
+ITER_RECORD = os.path.join(ROOT, "profiles", "iterations.json")
+# Jacobi-CG iterations to 1e-12 (3-2-1 BC) when no GPU run has recorded them yet
+DEFAULT_ITERS = {"cfg0_3x3": 374, "cfg1_10x10": 778}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=10, help="side of the CPU sample sub-array")
+    return ap.parse_args()
+
+
+def dist_info():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4) if r[5 + i] == "Active"})
+        loaded = [v for v in sm if v > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ inputs
+def build_inputs(cfg, device):
+    from paper_2411_12690_b200.api import build_config_rom
+    t = time.perf_counter()
+    rom_tsv = build_config_rom(cfg, 0, device)
+    rom_dum = build_config_rom(cfg, 1, device) if cfg.dummy_seed is not None else None
+    return rom_tsv, rom_dum, time.perf_counter() - t
+
+
+def make_stage(cfg, rom_tsv, rom_dum, device):
+    from paper_2411_12690_b200.api import ArrayLayout, GpuGlobalStage
+    g = GpuGlobalStage(device)
+    g.set_roms(rom_tsv, rom_dum)
+    layout = ArrayLayout(cfg.rows, cfg.cols, cfg.kinds(), cfg.delta_t(), cfg.p, cfg.h)
+    g.set_layout(layout)
+    g.set_bc(BC)
+    return g, layout
+
+
+# ------------------------------------------------------- CPU (reference)
+def cpu_sample(cfg, rom_tsv, rom_dum, iters, side, threads):
+    """Bounded sample of the reference's CPU path (oracle/_ref, unmodified
+    tsvstress sources) on a side x side sub-array of the same config and ROM:
+    index + assemble (CSR) + lifting, 30 Jacobi-CG iterations, recovery of
+    min(B_s, 50) blocks. Extrapolated per block to the full array with the
+    solve's iteration count (same CG, parity-tested)."""
+    from oracle import refpy
+    from paper_2411_12690_b200.api import save_rom
+    tmp = tempfile.mkdtemp(prefix="tsvbench_")
+
+    def as_ref(rom, name):
+        if rom is None or isinstance(rom, refpy.RefRom):
+            return rom
+        path = os.path.join(tmp, name)
+        save_rom(rom, path)  # byte-identical MRST file, read by the reference's load_rom
+        return refpy.load_rom(path)
+    r0, r1 = as_ref(rom_tsv, "tsv.rom"), as_ref(rom_dum, "dummy.rom")
+    Bs = side * side
+    kinds = cfg.kinds()
+    kinds_s = None if kinds is None else kinds.reshape(cfg.rows, cfg.cols)[:side, :side].ravel().copy()
+    dt = cfg.delta_t()
+    dt_s = dt if dt.size == 1 else dt.reshape(cfg.rows, cfg.cols)[:side, :side].ravel().copy()
+    t0 = time.perf_counter()
+    s = refpy.RefSession(r0, r1 if (kinds_s is not None and kinds_s.any()) else None, side, side,
+                         kinds=kinds_s, delta_t=dt_s, bc_mode=1)
+    t_setup = time.perf_counter() - t0
+    n_it = 30
+    t0 = time.perf_counter()
+    try:
+        s.iterate(1e-300, n_it, 1, threads)
+    except refpy.RefNoConvergence:
+        pass
+    t_solve = time.perf_counter() - t0
+    nrec = min(Bs, 50)
+    u = np.zeros(s.N)
+    t0 = time.perf_counter()
+    s.recover(u, cfg.points, 0, nrec, threads)
+    t_rec = time.perf_counter() - t0
+    per_block = t_setup / Bs + iters * (t_solve / n_it) / Bs + t_rec / nrec
+    total = per_block * cfg.B
+    for f in os.listdir(tmp):
+        os.remove(os.path.join(tmp, f))
+    os.rmdir(tmp)
+    return {"value": cfg.B / total, "unit": "blocks/s", "cores": threads, "kind": "reference",
+            "sample": (f"tsvstress CSR path (oracle/_ref) on a {side}x{side} sub-array of {cfg.name} with the same ROM: "
+                       f"index+assemble+lift {t_setup:.2f}s, {n_it} Jacobi-CG iterations {t_solve:.2f}s, recovery of "
+                       f"{nrec} blocks {t_rec:.2f}s; extrapolated per block to B={cfg.B} at {iters} iterations"),
+            "seconds_per_array": total}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import refpy
+    iters = json.load(open(ITER_RECORD)).get(cfg.name) if os.path.exists(ITER_RECORD) else None
+    iters = iters or DEFAULT_ITERS.get(cfg.name, 1)
+    threads = host_threads()
+    # the reference's own local stage (rom::build_rom) produces its input ROM
+    rom_tsv = refpy.build_rom(cfg.d, cfg.h, cfg.t, cfg.p, cfg.m_xy, cfg.m_z, cfg.q, 0, cfg.liner_e, threads)
+    rom_dum = (refpy.build_rom(cfg.d, cfg.h, cfg.t, cfg.p, cfg.m_xy, cfg.m_z, cfg.q, 1, cfg.liner_e, threads)
+               if cfg.dummy_seed is not None else None)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(cfg, rom_tsv, rom_dum, iters, args.cpu_sample, threads)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.median(x["value"] for x in vals)
+    line = {"metric": METRIC, "value": v, "unit": "blocks/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * cfg.B / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "blocks": cfg.B, "iterations": iters, "tol": TOL, "precond": "diagonal",
+                       "bc": BC, "points": cfg.points},
+            "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "blocks/s", "cores": threads, "kind": "reference",
+                             "sample": vals[-1]["sample"]},
+            "e2e": {"value": v, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args, cfg, rank, local_rank, world):
+    from paper_2411_12690_b200 import native
+    from paper_2411_12690_b200.api import ArrayLayout, IterOptions
+    L = native.load()
+    dev = local_rank
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(dev)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    rom_tsv, rom_dum, t_rom = build_inputs(cfg, dev)
+    g, layout = make_stage(cfg, rom_tsv, rom_dum, dev)
+    opts = IterOptions(TOL, 100000, "diagonal")
+    ix = g.index()
+
+    def step():
+        sol = g.solve_global(opts, copy_out=False)
+        g.recover_resident(cfg.points)
+        return sol, g.timing()
+
+    for _ in range(args.warmup):
+        sol, _ = step()
+    iters = sol.iterations
+    launches0 = g.timing().kernel_launches
+    barrier()
+    dev_ms = []
+    with ClockSampler(dev) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            sol, tm = step()
+            dev_ms.append(tm.solve_ms + tm.recover_ms)
+            iters = sol.iterations
+        wall = time.perf_counter() - t0
+    barrier()
+    launches = g.timing().kernel_launches - launches0
+    ms_step = max_over_ranks(sum(dev_ms) / len(dev_ms))
+    value = world * cfg.B / (ms_step / 1e3)
+    solve_ms, recover_ms = tm.solve_ms, tm.recover_ms
+
+    # dominant kernel (K1 operator apply) on its own stream, CUDA events
+    k1_ms = g.profile_apply(50)
+    k1_flops = 2.0 * cfg.n ** 2 * cfg.B
+    dmma_peak = ctypes_peak(L, dev)
+
+    # end to end through the C ABI with host buffers
+    e2e = run_e2e(args, cfg, g, layout, opts, L, world, max_over_ranks, barrier)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_sample(cfg, rom_tsv, rom_dum, iters, args.cpu_sample, host_threads())
+            cpu.pop("seconds_per_array", None)
+        except Exception as e:  # oracle not built: report, do not fail the bench
+            cpu = {"value": None, "unit": "blocks/s", "cores": host_threads(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    if rank == 0:
+        os.makedirs(os.path.dirname(ITER_RECORD), exist_ok=True)
+        rec = json.load(open(ITER_RECORD)) if os.path.exists(ITER_RECORD) else {}
+        rec[cfg.name] = iters
+        json.dump(rec, open(ITER_RECORD, "w"), indent=1, sort_keys=True)
+
+    flops_step = iters * 2.0 * cfg.n ** 2 * cfg.B + 2.0 * cfg.n_fine * cfg.n * cfg.B
+    out_bytes = cfg.B * cfg.elements * cfg.points * 7 * 8
+    hbm_peak = measured_hbm()
+    t_roof_ms = 1e3 * (iters * (2.0 * cfg.n ** 2 * cfg.B / (dmma_peak * 1e12) + 104.0 * ix.dof_count / (hbm_peak * 1e9))
+                       + max(2.0 * cfg.n_fine * cfg.n * cfg.B / (dmma_peak * 1e12), out_bytes / (hbm_peak * 1e9)))
+    line = {
+        "metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "blocks": cfg.B, "array": f"{cfg.rows}x{cfg.cols}", "reduced_dofs_per_block": cfg.n,
+                   "global_dofs": ix.dof_count, "fine_dofs_per_block": cfg.n_fine, "points_per_element": cfg.points,
+                   "iterations": iters, "tol": TOL, "precond": "diagonal", "bc": BC,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2: {out_bytes / 1e9:.1f} GB stress output + {ix.dof_count * 8 * 6 / 1e6:.0f} MB vectors per step"},
+        "roofline": {"bound": "tensor", "achieved": k1_flops / (k1_ms * 1e-3) / 1e12, "peak": dmma_peak,
+                     "unit": "TFLOP/s", "frac": k1_flops / (k1_ms * 1e-3) / 1e12 / dmma_peak, "traffic": None,
+                     "kernel": "gemm_nt_f64 (K1 operator apply, 2n^2 B FLOP per launch)",
+                     "peak_source": "measured live: register-only DMMA.8x8x4 loop (tsv_fp64_peak); MEASURED_PEAKS.json has no FP64 entry"},
+        "end_to_end_roofline": {"t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_step,
+                                "model": "iters*(2n^2B/P64 + 104N/BW) + max(2 n_fine n B/P64, 56 B/point/BW)",
+                                "hbm_gbs": hbm_peak},
+        "gflops": flops_step / (ms_step * 1e-3) / 1e9,
+        "phase_ms": {"solve": solve_ms, "recover": recover_ms, "k1_per_launch": k1_ms,
+                     "per_iteration": solve_ms / max(1, iters)},
+        "rom_build_s": t_rom,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_per_step": wall / args.steps,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def ctypes_peak(L, dev):
+    import ctypes as C
+    a, b = C.c_double(), C.c_double()
+    if L.tsv_fp64_peak(dev, C.byref(a), C.byref(b)) != 0:
+        return 37.16
+    return a.value
+
+
+def measured_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def run_e2e(args, cfg, g, layout, opts, L, world, max_over_ranks, barrier):
+    """Public API with host buffers: per step upload the layout (kinds, dT),
+    solve with u read back, recover every block into pinned host memory."""
+    import ctypes as C
+    from paper_2411_12690_b200.api import ArrayLayout
+    per_cell = cfg.elements * cfg.points * 7
+    out = np.empty((cfg.B, cfg.elements, cfg.points, 7))
+    L.tsv_host_register(out.ctypes.data_as(C.c_void_p), out.nbytes)
+    kinds = cfg.kinds()
+    dt = cfg.delta_t()
+    h2d = dt.nbytes + (kinds.nbytes if kinds is not None else 0)
+    d2h = out.nbytes + 8 * g.index().dof_count
+    try:
+        def e2e_step():
+            g.set_layout(ArrayLayout(cfg.rows, cfg.cols, kinds, dt, cfg.p, cfg.h))
+            g.set_bc(BC)
+            g.solve_global(opts, copy_out=True)
+            L.tsv_recover(g._h, cfg.points, 0, cfg.B, out.ctypes.data_as(C.c_void_p))
+        e2e_step()  # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        dt_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps)
+    finally:
+        L.tsv_host_unregister(out.ctypes.data_as(C.c_void_p))
+    assert np.isfinite(out[:, :, :, 6]).all()
+    return {"value": world * cfg.B / dt_s, "unit": "blocks/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "seconds_per_step": dt_s,
+            "path": "tsv_set_layout + tsv_set_bc + tsv_solve(u -> host) + tsv_recover(all cells -> pinned host)"}
+
+
+def main():
+    args = parse()
+    rank, local_rank, world = dist_info()
+    from paper_2411_12690_b200 import configs
+    cfg = configs.get(int(args.config) if args.config.isdigit() else args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+    return run_ours(args, cfg, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -159,6 +159,41 @@ int tsv_copy_stress(tsv_ctx *ctx, uint64_t cell_begin, uint64_t cell_end, double
 /* Reconstructed fine displacement of one cell (reconstruct_block_field). */
 int tsv_block_field(tsv_ctx *ctx, uint64_t cell, double *out /* n_fine */);
 
+/* One-shot local stage (rom::build_rom, rom.cpp:134-253) on the GPU: the
+ * reduced-order model of one unit block, i.e. the INPUT of the online
+ * stage, timed separately. Outputs are caller-allocated (sizes from
+ * tsv_rom_dims); any array pointer may be NULL. */
+typedef struct {
+    uint32_t q[3];          /* NodeLayout n_x, n_y, n_z */
+    double geometry[4];     /* d, h, t, p */
+    uint32_t grid_len[3];
+    const double *grid[3];  /* TensorGrid lines spanning [0,p]x[0,p]x[0,h] */
+    double materials[3][3]; /* E, nu, alpha per MaterialId */
+    int kind;               /* 0 tsv (materials by centroid radius), 1 dummy (all silicon) */
+} tsv_local_desc;
+
+typedef struct {
+    double *a_element;          /* n*n row-major */
+    double *b_element;          /* n */
+    double *basis;              /* n_fine*n row-major */
+    double *thermal;            /* n_fine */
+    uint8_t *element_material;  /* cells */
+    uint8_t fingerprint[32];    /* rom_fingerprint (rom.cpp:110-132) */
+    double build_ms;
+} tsv_rom_out;
+
+int tsv_rom_dims(const tsv_local_desc *desc, uint64_t *n, uint64_t *n_fine, uint64_t *cells);
+int tsv_build_rom(int device, const tsv_local_desc *desc, tsv_rom_out *out, char *err, size_t err_len);
+
+/* Page-lock a host buffer so tsv_recover / tsv_solve copies run at full
+ * PCIe/C2C rate (cudaHostRegister); unregister before freeing it. */
+int tsv_host_register(void *ptr, size_t bytes);
+int tsv_host_unregister(void *ptr);
+
+/* FP64 roofline denominators measured live on `device`: register-only
+ * DMMA.8x8x4 (mma.sync f64) and DFMA issue loops over all SMs. */
+int tsv_fp64_peak(int device, double *dmma_tflops, double *dfma_tflops);
+
 /* Measurement hooks: time `reps` K1 launches alone; read timings. */
 int tsv_profile_apply(tsv_ctx *ctx, int reps, double *ms_per_launch);
 int tsv_get_timing(tsv_ctx *ctx, tsv_timing *out);

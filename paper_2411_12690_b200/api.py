@@ -296,3 +296,129 @@ class GpuGlobalStage:
         t = Timing()
         self._check(self._L.tsv_get_timing(self._h, C.byref(t)))
         return t
+
+
+def build_rom(q, geometry, grid, materials, kind: int = 0, device: int = 0) -> ReducedOrderModel:
+    """One-shot local stage on the GPU (rom::build_rom, rom.cpp:134-253):
+    the ROM of one unit block. Input of the online stage; timed separately
+    (``ReducedOrderModel.build_ms``)."""
+    L = native.load()
+    d = native.LocalDesc()
+    d.q[:] = [int(v) for v in (q if not np.isscalar(q) else (q, q, q))]
+    d.geometry[:] = [float(v) for v in geometry]
+    grids = [np.ascontiguousarray(g, np.float64) for g in grid]
+    d.grid_len[:] = [len(g) for g in grids]
+    for a in range(3):
+        d.grid[a] = _p(grids[a])
+    mats = np.asarray(materials, np.float64)
+    for i in range(3):
+        for j in range(3):
+            d.materials[i][j] = float(mats[i, j])
+    d.kind = int(kind)
+    n, nf, cells = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    rc = L.tsv_rom_dims(C.byref(d), C.byref(n), C.byref(nf), C.byref(cells))
+    if rc != TSV_OK:
+        raise Error(f"build_rom: invalid descriptor (status {rc})")
+    K = np.empty((n.value, n.value)); b = np.empty(n.value); Phi = np.empty((nf.value, n.value))
+    uT = np.empty(nf.value); em = np.empty(cells.value, np.uint8)
+    out = native.RomOut()
+    out.a_element, out.b_element, out.basis, out.thermal, out.element_material = \
+        _p(K), _p(b), _p(Phi), _p(uT), _p(em)
+    err = C.create_string_buffer(512)
+    rc = L.tsv_build_rom(device, C.byref(d), C.byref(out), err, 512)
+    if rc != TSV_OK:
+        raise Error(f"build_rom: {err.value.decode()}")
+    rom = ReducedOrderModel(q=tuple(d.q), geometry=tuple(geometry), grid=tuple(grids), materials=mats[:, :3].copy(),
+                            a_element=K, b_element=b, basis=Phi, thermal=uT, element_material=em,
+                            fingerprint=bytes(out.fingerprint), kind=int(kind))
+    rom.build_ms = out.build_ms
+    return rom
+
+
+def build_config_rom(cfg, kind: int = 0, device: int = 0) -> ReducedOrderModel:
+    """ROM of a configs.TsvConfig unit block on its uniform grid."""
+    # linspace with exact end points, as tsvstress::linspace (core.cpp:14-22)
+    grid = tuple(np.array([0.0] + [a + (b - a) * i / m for i in range(1, m)] + [b]) for (a, b, m) in
+                 ((0.0, cfg.p, cfg.m_xy), (0.0, cfg.p, cfg.m_xy), (0.0, cfg.h, cfg.m_z)))
+    return build_rom(cfg.q, (cfg.d, cfg.h, cfg.t, cfg.p), grid, cfg.materials(), kind, device)
+
+
+# ------------------------------------------------------------ .rom files
+# The reference's "MRST" v1 little-endian format (rom.cpp:257-377): magic,
+# version, kind byte, header (geometry, grid lines, materials, layout), the
+# SHA-256 of the header, then the column-major basis, thermal, a_element,
+# b_element.
+_MAGIC = b"MRST"
+
+
+def _rom_header(rom: ReducedOrderModel) -> bytes:
+    import struct
+    out = bytearray()
+    out += struct.pack("<4d", *[float(v) for v in rom.geometry])
+    for g in rom.grid:
+        g = np.ascontiguousarray(g, "<f8")
+        out += struct.pack("<I", len(g)) + g.tobytes()
+    mats = np.asarray(rom.materials, np.float64)
+    for i in range(3):
+        out += struct.pack("<B3d", i, *[float(v) for v in mats[i, :3]])
+    out += struct.pack("<3I", *[int(v) for v in rom.q])
+    return bytes(out)
+
+
+def save_rom(rom: ReducedOrderModel, path: str) -> None:
+    """save_rom (rom.cpp:262-303)."""
+    import hashlib
+    import struct
+    hdr = _rom_header(rom)
+    fp = hashlib.sha256(hdr).digest()
+    with open(path, "wb") as f:
+        f.write(_MAGIC + struct.pack("<IB", 1, int(rom.kind)) + hdr + fp)
+        f.write(np.asfortranarray(np.asarray(rom.basis, "<f8")).tobytes(order="F"))
+        for a in (rom.thermal, rom.a_element, rom.b_element):
+            f.write(np.ascontiguousarray(a, "<f8").tobytes())
+
+
+def load_rom(path: str) -> ReducedOrderModel:
+    """load_rom (rom.cpp:305-377): validates magic, version, kind, the
+    header fingerprint and the body length."""
+    import hashlib
+    import struct
+    data = open(path, "rb").read()
+    if data[:4] != _MAGIC:
+        raise Error(f"load_rom: {path} is not a ROM file (bad magic)")
+    version, kind = struct.unpack_from("<IB", data, 4)
+    if version != 1:
+        raise Error(f"load_rom: {path} has unsupported format version {version}")
+    if kind > 1:
+        raise Error("load_rom: invalid block kind byte")
+    pos = 9
+    geom = struct.unpack_from("<4d", data, pos); pos += 32
+    grid = []
+    for _ in range(3):
+        (ln,) = struct.unpack_from("<I", data, pos); pos += 4
+        if ln < 2 or ln > 100000000:
+            raise Error("load_rom: corrupt grid axis length")
+        grid.append(np.frombuffer(data, "<f8", ln, pos).copy()); pos += 8 * ln
+    mats = np.zeros((3, 3))
+    for i in range(3):
+        mid, e, nu, al = struct.unpack_from("<B3d", data, pos); pos += 25
+        if mid != i:
+            raise Error("load_rom: material table out of order")
+        mats[i] = (e, nu, al)
+    q = struct.unpack_from("<3I", data, pos); pos += 12
+    fp = data[pos:pos + 32]
+    if hashlib.sha256(data[9:pos]).digest() != fp:
+        raise Error(f"load_rom: {path} fingerprint does not match its header (corrupt file)")
+    pos += 32
+    nf = 3 * len(grid[0]) * len(grid[1]) * len(grid[2])
+    n = 3 * (q[0] * q[1] * q[2] - (q[0] - 2) * (q[1] - 2) * (q[2] - 2))
+    body = (nf * n + nf + n * n + n) * 8
+    if len(data) - pos != body:
+        raise Error(f"load_rom: {path}: corrupt length (body is {len(data) - pos} bytes, expected {body})")
+    basis = np.frombuffer(data, "<f8", nf * n, pos).reshape(n, nf).T.copy(); pos += 8 * nf * n
+    thermal = np.frombuffer(data, "<f8", nf, pos).copy(); pos += 8 * nf
+    K = np.frombuffer(data, "<f8", n * n, pos).reshape(n, n).copy(); pos += 8 * n * n
+    b = np.frombuffer(data, "<f8", n, pos).copy()
+    return ReducedOrderModel(q=tuple(q), geometry=tuple(geom), grid=tuple(grid), materials=mats, a_element=K,
+                             b_element=b, basis=basis, thermal=thermal, element_material=None, fingerprint=fp,
+                             kind=kind)

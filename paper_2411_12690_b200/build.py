@@ -22,7 +22,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O3",
     "--expt-relaxed-constexpr",
 ]
-SOURCES = ["context.cu", "host_index.cpp"]
+SOURCES = ["context.cu", "local_stage.cu", "host_index.cpp"]
+LIBS = ["-lcusolver", "-lcublas", "-lcrypto", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 
 
 def _nvcc():
@@ -54,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs, *LIBS]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

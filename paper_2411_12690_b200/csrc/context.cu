@@ -679,6 +679,43 @@ extern "C" {
 
 int tsv_abi_version(void) { return TSV_B200_ABI_VERSION; }
 
+int tsv_host_register(void *ptr, size_t bytes) {
+    return cudaHostRegister(ptr, bytes, cudaHostRegisterDefault) == cudaSuccess ? TSV_OK : TSV_ECUDA;
+}
+
+int tsv_host_unregister(void *ptr) { return cudaHostUnregister(ptr) == cudaSuccess ? TSV_OK : TSV_ECUDA; }
+
+int tsv_fp64_peak(int device, double *dmma_tflops, double *dfma_tflops) {
+    if (cudaSetDevice(device) != cudaSuccess) return TSV_ECUDA;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    double *sink = nullptr;
+    if (cudaMalloc(&sink, sizeof(double)) != cudaSuccess) return TSV_ENOMEM;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4000, warps = 16;
+    float ms = 0.f;
+    peak_dmma_kernel<<<sms, 32 * warps>>>(sink, 64);
+    cudaEventRecord(e0);
+    peak_dmma_kernel<<<sms, 32 * warps>>>(sink, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (dmma_tflops) *dmma_tflops = 2.0 * 256 * 8 * iters * double(sms) * warps / ms / 1e9;
+    peak_dfma_kernel<<<sms, 32 * warps>>>(sink, 64);
+    cudaEventRecord(e0);
+    peak_dfma_kernel<<<sms, 32 * warps>>>(sink, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (dfma_tflops) *dfma_tflops = 2.0 * 16 * iters * double(sms) * 32 * warps / ms / 1e9;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    return cudaGetLastError() == cudaSuccess ? TSV_OK : TSV_ECUDA;
+}
+
 int tsv_index_global_nodes(uint32_t rows, uint32_t cols, const uint32_t q[3], uint64_t *n_dofs, uint32_t lattice[3],
                            int32_t *nol, uint32_t *lon, uint32_t *dm) {
     try {

@@ -607,4 +607,33 @@ __global__ void stress_kernel(StressParams sp) {
     }
 }
 
+// ------------------------------------------------------------ peaks
+__global__ void peak_dmma_kernel(double *sink, int iters) {
+    double acc[8][2];
+    const double a = threadIdx.x * 1e-9, b = 1.0 + threadIdx.x * 1e-12;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma_8x8x4(acc[i][0], acc[i][1], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += acc[i][0] + acc[i][1];
+    if (s == 12345.0) sink[0] = s;
+}
+
+__global__ void peak_dfma_kernel(double *sink, int iters) {
+    double acc[16];
+    const double a = threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-12;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = i;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = fma(acc[i], b, a);
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i];
+    if (s == 12345.0) sink[0] = s;
+}
+
 }  // namespace tsvb200

@@ -19,6 +19,7 @@ EXPORTS = [
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
     "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_solve", "tsv_set_solution", "tsv_recover",
     "tsv_recover_resident", "tsv_copy_stress", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
+    "tsv_rom_dims", "tsv_build_rom", "tsv_host_register", "tsv_host_unregister", "tsv_fp64_peak",
 ]
 
 
@@ -45,6 +46,17 @@ class IterOptionsC(C.Structure):
 class SolveInfo(C.Structure):
     _fields_ = [("iterations", C.c_int), ("relative_residual", C.c_double), ("direct_fallback", C.c_int),
                 ("best_iterations", C.c_int), ("solve_ms", C.c_double), ("kernel_launches", C.c_uint64)]
+
+
+class LocalDesc(C.Structure):
+    _fields_ = [("q", C.c_uint32 * 3), ("geometry", C.c_double * 4), ("grid_len", C.c_uint32 * 3),
+                ("grid", C.c_void_p * 3), ("materials", (C.c_double * 3) * 3), ("kind", C.c_int)]
+
+
+class RomOut(C.Structure):
+    _fields_ = [("a_element", C.c_void_p), ("b_element", C.c_void_p), ("basis", C.c_void_p),
+                ("thermal", C.c_void_p), ("element_material", C.c_void_p), ("fingerprint", C.c_uint8 * 32),
+                ("build_ms", C.c_double)]
 
 
 class Timing(C.Structure):
@@ -91,6 +103,11 @@ def load(path: str = LIB_PATH):
         "tsv_block_field": (i, [vp, u64, vp]),
         "tsv_profile_apply": (i, [vp, i, P(d)]),
         "tsv_get_timing": (i, [vp, P(Timing)]),
+        "tsv_host_register": (i, [vp, sz]),
+        "tsv_host_unregister": (i, [vp]),
+        "tsv_fp64_peak": (i, [i, P(d), P(d)]),
+        "tsv_rom_dims": (i, [P(LocalDesc), P(u64), P(u64), P(u64)]),
+        "tsv_build_rom": (i, [i, P(LocalDesc), P(RomOut), C.c_char_p, sz]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
