@@ -32,6 +32,7 @@ namespace {
 
 using K1Cfg = GemmCfg<128, 64, 2, 2, 16, 3>;
 using K6Cfg = GemmCfg<128, 64, 2, 2, 16, 3>;
+using K1SmallCfg = GemmCfg<64, 64, 2, 2, 16, 3, 3>;  // KC must divide ldk (multiple of 16)
 constexpr int kBM = K1Cfg::BM;
 constexpr int kBN = K1Cfg::BN;
 constexpr int kKC = K1Cfg::KC;
@@ -126,7 +127,7 @@ struct tsv_ctx {
     // device
     DevBuf<double> X, Y, b, x, r, p, ap, pre, partial, row_dt_d, U, stress;
     DevBuf<int> slots, row_cell_d;
-    DevBuf<uint8_t> cmask, row_kind_d, tile_kind_d;
+    DevBuf<uint8_t> cmask, row_kind_d, tile_kind_d, tile_kind_small_d;
     DevBuf<unsigned> tile_counter;
     DevBuf<CgState> state;
     int pre_kind = -1;
@@ -136,6 +137,8 @@ struct tsv_ctx {
 
     cudaGraphExec_t iter_graph = nullptr;
     int k1_grid = 0, k6_grid = 0;
+    int k1s_grid = 0;
+    bool k1_small = false;  // small arrays: 64 x 64 tiles keep every SM busy
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
@@ -218,6 +221,9 @@ struct tsv_ctx {
         for (size_t j = 0; j < B_pad; ++j)
             if (row_cell[j] >= 0) cell_row[row_cell[j]] = static_cast<int>(j);
 
+        // Few 128 x 64 tiles (small arrays): switch K1 to 64 x 64 tiles.
+        k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(3 * k1_grid);
+
         // Block-major node renumbering + slot table.
         const size_t nn = nl.node_count();
         node_int_of_glob.assign(nodes, 0xffffffffu);
@@ -253,6 +259,12 @@ struct tsv_ctx {
         row_cell_d.upload(row_cell.data(), row_cell.size(), s);
         row_kind_d.upload(row_kind.data(), row_kind.size(), s);
         tile_kind_d.upload(tile_kind.data(), tile_kind.size(), s);
+        {
+            std::vector<uint8_t> tks;
+            for (uint8_t k : tile_kind)
+                for (int i = 0; i < kBM / K1SmallCfg::BM; ++i) tks.push_back(k);
+            tile_kind_small_d.upload(tks.data(), tks.size(), s);
+        }
         row_dt_d.upload(row_dt.data(), row_dt.size(), s);
         X.alloc(B_pad * ldk);
         Y.alloc(B_pad * ldk);
@@ -401,6 +413,9 @@ struct tsv_ctx {
 
     // ------------------------------------------------------------ kernels
     unsigned vec_grid() const { return static_cast<unsigned>(std::max<size_t>(1, (nodes + kVecThreads - 1) / kVecThreads)); }
+    // CG vector kernels: fixed grid (grid-stride), so the per-CTA partials
+    // and their fixed-order sum stay small and deterministic.
+    unsigned cg_grid() const { return std::min<unsigned>(vec_grid(), static_cast<unsigned>(sm_count) * 8u); }
 
     void launch_scatter(const double *v, int mode) {
         scatter_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), slots.ptr, cmask.ptr, v,
@@ -432,7 +447,15 @@ struct tsv_ctx {
 
     void launch_k1(const int *done) {
         GemmParams gp = k1_params(done);
-        gemm_nt_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp);
+        if (k1_small) {
+            gp.m_tiles = static_cast<int>(B_pad / K1SmallCfg::BM);
+            gp.n_tiles = static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
+            gp.k_chunks = static_cast<int>(ldk / K1SmallCfg::KC);
+            gp.tile_kind = tile_kind_small_d.ptr;
+            gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+        } else {
+            gemm_nt_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp);
+        }
         ++launches;
         CK(cudaGetLastError());
     }
@@ -458,9 +481,9 @@ struct tsv_ctx {
 
     void launch_iteration(const CgParams &q) {
         launch_k1(&state.ptr->done);
-        cg_gather_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
-        cg_update_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
-        cg_scatter_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        cg_gather_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
         launches += 3;
     }
 
@@ -548,8 +571,8 @@ struct tsv_ctx {
         CK(cudaMemcpyAsync(state.ptr, h_state, sizeof(CgState), cudaMemcpyHostToDevice, stream));
         CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), stream));
         CgParams q = cg_params();
-        cg_update_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
-        cg_scatter_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(q);
+        cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
         launches += 2;
         CK(cudaGetLastError());
         // Host-polled batches of graph-captured iterations; a finished
@@ -763,6 +786,12 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1Cfg::SMEM)));
+        CK(cudaFuncSetAttribute(gemm_nt_f64<K1SmallCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K1SmallCfg::SMEM)));
+        int occ_s = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, gemm_nt_f64<K1SmallCfg>, K1SmallCfg::THREADS,
+                                                         K1SmallCfg::SMEM));
+        ctx->k1s_grid = std::max(1, occ_s) * ctx->sm_count;
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_nt_f64<K1Cfg>, K1Cfg::THREADS, K1Cfg::SMEM));
         ctx->k1_grid = ctx->k6_grid = std::max(1, occ) * ctx->sm_count;

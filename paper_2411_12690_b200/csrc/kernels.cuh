@@ -47,14 +47,14 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int WM_, int WN_, int KC_, int STAGES_>
+template <int BM_, int BN_, int WM_, int WN_, int KC_, int STAGES_, int MINB_ = 2>
 struct GemmCfg {
-    static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, KC = KC_, STAGES = STAGES_;
+    static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, KC = KC_, STAGES = STAGES_, MINB = MINB_;
     static constexpr int THREADS = WM * WN * 32;
     static constexpr int TM = BM / WM, TN = BN / WN, FM = TM / 8, FN = TN / 8;
     // Row pitch KC+4 doubles: 8-byte fragment loads of a half-warp (4 rows x
@@ -83,11 +83,46 @@ __device__ __forceinline__ void gemm_load_stage(double *As, double *Bs, const do
     }
 }
 
+// One KC-deep chunk of warp-tile DMMAs from shared memory; NJ n-fragments.
+template <class Cfg, int NJ>
+__device__ __forceinline__ void mma_chunk(double (&acc)[Cfg::FM][Cfg::FN][2], const double *as, const double *bs) {
+#pragma unroll
+    for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
+        double af[Cfg::FM], bf[NJ];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[i * 8 * Cfg::SP + ks * 4];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) bf[j] = bs[j * 8 * Cfg::SP + ks * 4];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int i = 0; i < Cfg::FM; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+}
+
+template <class Cfg>
+__device__ __forceinline__ void mma_chunk_partial(double (&acc)[Cfg::FM][Cfg::FN][2], const double *as, const double *bs,
+                                               int fn_lim) {
+    for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
+        double af[Cfg::FM];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) af[i] = as[i * 8 * Cfg::SP + ks * 4];
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) {
+            if (j < fn_lim) {
+                const double bf = bs[j * 8 * Cfg::SP + ks * 4];
+#pragma unroll
+                for (int i = 0; i < Cfg::FM; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf);
+            }
+        }
+    }
+}
+
 // Persistent DMMA GEMM: grid = resident CTAs, tiles handed out by an atomic
 // counter (M tile major, N tile minor, so concurrently running CTAs share
 // the streamed A panel in L2).
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 2) gemm_nt_f64(GemmParams p) {
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParams p) {
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_tile;
     double *As = smem;
@@ -134,21 +169,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 2) gemm_nt_f64(GemmParams p) {
             cp_async_commit();
             const double *as = As + (kc % Cfg::STAGES) * Cfg::A_STAGE + (wm * Cfg::TM + (lane >> 2)) * Cfg::SP + (lane & 3);
             const double *bs = Bs + (kc % Cfg::STAGES) * Cfg::B_STAGE + (wn * Cfg::TN + (lane >> 2)) * Cfg::SP + (lane & 3);
-#pragma unroll
-            for (int ks = 0; ks < Cfg::KC / 4; ++ks) {
-                double af[Cfg::FM], bf[Cfg::FN];
-#pragma unroll
-                for (int i = 0; i < Cfg::FM; ++i) af[i] = as[i * 8 * Cfg::SP + ks * 4];
-#pragma unroll
-                for (int j = 0; j < Cfg::FN; ++j) bf[j] = bs[j * 8 * Cfg::SP + ks * 4];
-#pragma unroll
-                for (int j = 0; j < Cfg::FN; ++j) {
-                    if (j < fn_lim) {
-#pragma unroll
-                        for (int i = 0; i < Cfg::FM; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-                    }
-                }
-            }
+            if (fn_lim == Cfg::FN)
+                mma_chunk<Cfg, Cfg::FN>(acc, as, bs);
+            else if (fn_lim > 0)
+                mma_chunk_partial<Cfg>(acc, as, bs, fn_lim);
         }
         cp_async_wait<0>();
         __syncthreads();
@@ -248,16 +272,18 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *sh /* [32*NV]
     }
 }
 
-// Sum of per-CTA partials in CTA order by one warp (the last CTA of a grid).
+// Sum of per-CTA partials (CTA order, fixed strides and tree): every thread
+// of the last CTA takes a strided subset, then a block tree. Deterministic
+// for a fixed grid; result valid in thread 0.
 template <int NV>
-__device__ __forceinline__ void grid_sum(const double *partial, int nblocks, double (&out)[NV]) {
-    const int lane = threadIdx.x & 31;
+__device__ __forceinline__ void grid_sum(const double *partial, int nblocks, double (&out)[NV], double *sh) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
         double s = 0.0;
-        for (int k = lane; k < nblocks; k += 32) s += partial[k * NV + i];
-        out[i] = warp_sum(s);
+        for (int k = threadIdx.x; k < nblocks; k += blockDim.x) s += partial[k * NV + i];
+        out[i] = s;
     }
+    block_sum<NV>(out, sh);
 }
 
 __device__ __forceinline__ void precond_node(int kind, const double *pre, int node, const double r[3], double z[3]) {
@@ -275,16 +301,30 @@ __device__ __forceinline__ void precond_node(int kind, const double *pre, int no
     }
 }
 
-// A: Y (= A p or A x) summed per owned DoF; p'Ap or the true residual.
-__global__ void cg_gather_kernel(CgParams q) {
-    __shared__ double sh[64];
+// Publish this CTA's partials; returns true in every thread of the last CTA.
+template <int NV>
+__device__ __forceinline__ bool publish_partials(const double (&v)[NV], double *partial, unsigned *ticket) {
     __shared__ bool last;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) partial[blockIdx.x * NV + i] = v[i];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+// A: Y (= A p or A x) summed per owned DoF; p'Ap or the true residual.
+// Grid-stride over nodes with a fixed grid (deterministic reduction).
+__global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
+    __shared__ double sh[64];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int yx = st->y_holds_x;
-    const int node = blockIdx.x * blockDim.x + threadIdx.x;
     double part[1] = {0.0};
-    if (node < q.n_nodes) {
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < q.n_nodes; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -310,16 +350,9 @@ __global__ void cg_gather_kernel(CgParams q) {
         }
     }
     block_sum<1>(part, sh);
-    if (threadIdx.x == 0) {
-        q.partial[blockIdx.x] = part[0];
-        __threadfence();
-        last = atomicAdd(&st->ticket_a, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last || threadIdx.x >= 32) return;
-    __threadfence();
+    if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
     double tot[1];
-    grid_sum<1>(q.partial, gridDim.x, tot);
+    grid_sum<1>(q.partial, gridDim.x, tot, sh);
     if (threadIdx.x == 0) {
         st->ticket_a = 0u;
         if (!yx) {
@@ -346,16 +379,14 @@ __global__ void cg_gather_kernel(CgParams q) {
 // B: x += alpha p, r -= alpha Ap, z = M r, (r.z, r.r); or the restart /
 // initial variants. The last CTA advances the iteration counter and
 // decides what the next operator product is (loop head of cg_solve).
-__global__ void cg_update_kernel(CgParams q) {
+__global__ void __launch_bounds__(256) cg_update_kernel(CgParams q) {
     __shared__ double sh[64];
-    __shared__ bool last;
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int phase = st->phase;
     const double alpha = st->alpha;
-    const int node = blockIdx.x * blockDim.x + threadIdx.x;
     double part[2] = {0.0, 0.0};
-    if (node < q.n_nodes) {
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < q.n_nodes; node += gridDim.x * blockDim.x) {
         double r3[3], z3[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -382,17 +413,9 @@ __global__ void cg_update_kernel(CgParams q) {
         }
     }
     block_sum<2>(part, sh);
-    if (threadIdx.x == 0) {
-        q.partial[2 * blockIdx.x] = part[0];
-        q.partial[2 * blockIdx.x + 1] = part[1];
-        __threadfence();
-        last = atomicAdd(&st->ticket_b, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last || threadIdx.x >= 32) return;
-    __threadfence();
+    if (!publish_partials<2>(part, q.partial, &st->ticket_b)) return;
     double tot[2];
-    grid_sum<2>(q.partial, gridDim.x, tot);
+    grid_sum<2>(q.partial, gridDim.x, tot, sh);
     if (threadIdx.x != 0) return;
     st->ticket_b = 0u;
     if (phase == PH_INIT) {
@@ -443,32 +466,32 @@ __global__ void cg_update_kernel(CgParams q) {
 
 // C: p = z + beta p (or p = z), then write the next operator operand (p,
 // or x for a verification) into the block-major panel, free DoFs only.
-__global__ void cg_scatter_kernel(CgParams q) {
+__global__ void __launch_bounds__(256) cg_scatter_kernel(CgParams q) {
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
-    const int node = blockIdx.x * blockDim.x + threadIdx.x;
-    if (node >= q.n_nodes) return;
     const int p_assign = st->p_assign, yx = st->y_holds_x;
     const double beta = st->beta;
-    double r3[3], z3[3], v[3];
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < q.n_nodes; node += gridDim.x * blockDim.x) {
+        double r3[3], z3[3], v[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) r3[c] = q.r[3LL * node + c];
-    precond_node(q.precond, q.pre, node, r3, z3);
+        for (int c = 0; c < 3; ++c) r3[c] = q.r[3LL * node + c];
+        precond_node(q.precond, q.pre, node, r3, z3);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const long long dof = 3LL * node + c;
-        const double pn = p_assign ? z3[c] : z3[c] + beta * q.p[dof];
-        q.p[dof] = pn;
-        v[c] = yx ? q.x[dof] : pn;
-    }
-    const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
-    const int sl[4] = {s.x, s.y, s.z, s.w};
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = 3LL * node + c;
+            const double pn = p_assign ? z3[c] : z3[c] + beta * q.p[dof];
+            q.p[dof] = pn;
+            v[c] = yx ? q.x[dof] : pn;
+        }
+        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+        const int sl[4] = {s.x, s.y, s.z, s.w};
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        if (q.cmask[3LL * node + c]) continue;
+        for (int c = 0; c < 3; ++c) {
+            if (q.cmask[3LL * node + c]) continue;
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (sl[k] >= 0) q.X[sl[k] + c] = v[c];
+            for (int k = 0; k < 4; ++k)
+                if (sl[k] >= 0) q.X[sl[k] + c] = v[c];
+        }
     }
 }
 
