@@ -419,3 +419,34 @@ int ref_session_block_field(void* h, const double* u, uint64_t cell, double* out
 }
 
 }  // extern "C"
+
+extern "C" {
+
+/// index_global_nodes + GlobalIndex::global_dof alone (no assembly), for
+/// bit-exact index checks at sizes where assemble_global would need ~100 GB.
+/// Returns the dof count; dof_map [rows*cols][n] may be NULL.
+int64_t ref_index(uint32_t rows, uint32_t cols, uint32_t q, uint32_t *dof_map) {
+    int64_t n_dofs = -1;
+    guarded([&] {
+        global::ArrayLayout layout;
+        layout.rows = rows;
+        layout.cols = cols;
+        layout.delta_t = {0.0};
+        layout.pitch = 1.0;
+        layout.height = 1.0;
+        rom::NodeLayout nl = rom::NodeLayout::create(q, q, q, 1.0, 1.0, 1.0);
+        global::GlobalIndex idx = global::index_global_nodes(layout, nl);
+        n_dofs = static_cast<int64_t>(idx.dof_count());
+        if (dof_map) {
+            const std::size_t n = nl.reduced_dofs();
+            for (std::uint32_t r = 0; r < rows; ++r)
+                for (std::uint32_t c = 0; c < cols; ++c) {
+                    std::size_t b = static_cast<std::size_t>(r) * cols + c;
+                    for (std::size_t a = 0; a < n; ++a) dof_map[b * n + a] = idx.global_dof(r, c, nl, a);
+                }
+        }
+    });
+    return n_dofs;
+}
+
+}  // extern "C"

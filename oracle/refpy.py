@@ -233,3 +233,17 @@ class RefSession:
         if lib().ref_session_block_field(self.h, _ptr(u), cell, _ptr(out)) != 0:
             raise RefError(_err())
         return out
+
+
+def index_dof_map(rows, cols, q):
+    """The reference's index_global_nodes / global_dof (no assembly)."""
+    L = lib()
+    L.ref_index.restype = C.c_int64
+    L.ref_index.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]
+    nd = L.ref_index(rows, cols, q, None)
+    if nd < 0:
+        raise RefError(_err())
+    n = 3 * (q ** 3 - (q - 2) ** 3)
+    out = np.empty((rows * cols, n), np.uint32)
+    L.ref_index(rows, cols, q, _ptr(out))
+    return nd, out

@@ -230,16 +230,3 @@ def test_nan_load_is_a_breakdown(oracle_libs, native_lib):
     _, g = make_case(refpy, configs.get(0), 2, 2, dts=[float("nan")])
     with pytest.raises(BreakdownError):
         g.solve_global(IterOptions(1e-12))
-
-
-@pytest.mark.slow
-def test_config1_full_parity(oracle_libs, native_lib):
-    refpy, _ = oracle_libs
-    sess, g = make_case(refpy, configs.get(1))
-    assert np.array_equal(g.dof_map(), sess.dof_map())
-    u_r, it_r, _ = sess.iterate(1e-12)
-    sol = g.solve_global(IterOptions(1e-12))
-    assert rel_l2(sol.u, u_r) <= U_TOL
-    s_ref = sess.recover(u_r, 8)
-    mx, l2 = stress_errors(g.recover(8), s_ref)
-    assert mx.max() <= S_TOL and l2.max() <= S_TOL
