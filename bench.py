@@ -243,7 +243,7 @@ def run_ours(args, cfg, rank, local_rank, world):
         g.recover_resident(cfg.points)
         return sol, g.timing()
 
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):
         sol, _ = step()
     iters = sol.iterations
     launches0 = g.timing().kernel_launches
@@ -268,7 +268,7 @@ def run_ours(args, cfg, rank, local_rank, world):
     dmma_peak = ctypes_peak(L, dev)
 
     # end to end through the C ABI with host buffers
-    e2e = run_e2e(args, cfg, g, layout, opts, L, world, max_over_ranks, barrier)
+    e2e = run_e2e(args, cfg, g, layout, opts, L, world, max_over_ranks, barrier) if args.e2e_steps > 0 else None
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
