@@ -222,7 +222,7 @@ struct tsv_ctx {
             if (row_cell[j] >= 0) cell_row[row_cell[j]] = static_cast<int>(j);
 
         // Few 128 x 64 tiles (small arrays): switch K1 to 64 x 64 tiles.
-        k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(3 * k1_grid);
+        k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(k1_grid);  // fewer tiles than CTA slots
 
         // Block-major node renumbering + slot table.
         const size_t nn = nl.node_count();
