@@ -80,6 +80,10 @@ struct DevBuf {
 
 size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
 
+// Panel column of local reduced DoF a = 3 rank + c (rom.cpp:26-31 order):
+// component-major within a block row.
+inline size_t pidx(size_t a, size_t nn) { return (a % 3) * nn + a / 3; }
+
 struct RomHost {
     bool set = false;
     uint32_t q[3] = {0, 0, 0};
@@ -245,7 +249,7 @@ struct tsv_ctx {
                 int k = 0;
                 while (k < 4 && s[k] >= 0) ++k;
                 if (k == 4) throw StatusError(TSV_EINVAL, "index: a reduced node is shared by more than 4 blocks");
-                s[k] = static_cast<int>(j * ldk + 3 * rank);
+                s[k] = static_cast<int>(j * ldk + rank);  // + c * nn per component
             }
         }
         if (node_glob_of_int.size() != nodes) throw StatusError(TSV_EINVAL, "index: unreferenced global node");
@@ -292,7 +296,7 @@ struct tsv_ctx {
             if (constrained[i] && g[i] != 0.0) any_g = true;
         std::vector<uint8_t> cm_int(N);
         for (size_t in = 0; in < nodes; ++in)
-            for (int c = 0; c < 3; ++c) cm_int[3 * in + c] = constrained[3 * node_glob_of_int[in] + c];
+            for (int c = 0; c < 3; ++c) cm_int[c * nodes + in] = constrained[3 * node_glob_of_int[in] + c];
         cmask.upload(cm_int.data(), N, stream);
         bc_set = true;
         pre_kind = -1;
@@ -304,13 +308,13 @@ struct tsv_ctx {
     std::vector<T> to_internal(const T *v) const {
         std::vector<T> out(N);
         for (size_t in = 0; in < nodes; ++in)
-            for (int c = 0; c < 3; ++c) out[3 * in + c] = v[3 * node_glob_of_int[in] + c];
+            for (int c = 0; c < 3; ++c) out[c * nodes + in] = v[3 * node_glob_of_int[in] + c];
         return out;
     }
     template <typename T>
     void to_reference(const T *v_int, T *out) const {
         for (size_t in = 0; in < nodes; ++in)
-            for (int c = 0; c < 3; ++c) out[3 * node_glob_of_int[in] + c] = v_int[3 * in + c];
+            for (int c = 0; c < 3; ++c) out[3 * node_glob_of_int[in] + c] = v_int[c * nodes + in];
     }
 
     // Assembled load (global_stage.cpp:135-142, cell order, bit-exact) and
@@ -332,7 +336,7 @@ struct tsv_ctx {
             r.upload(gi.data(), N, stream);
             launch_scatter(r.ptr, 2);
             launch_k1(nullptr);
-            gather_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), slots.ptr, cmask.ptr,
+            gather_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), static_cast<int>(n / 3), slots.ptr, cmask.ptr,
                                                                     Y.ptr, b.ptr, b.ptr, 1);
             ++launches;
             CK(cudaGetLastError());
@@ -401,7 +405,7 @@ struct tsv_ctx {
                     inv[8] = (m[0] * m[4] - m[1] * m[3]) / det;
                 }
                 const size_t in = node_int_of_glob[node];
-                std::memcpy(inv_int.data() + in * 9, inv, sizeof(inv));
+                for (int k = 0; k < 9; ++k) inv_int[k * nodes + in] = inv[k];
             }
             pre.upload(inv_int.data(), inv_int.size(), stream);
         } else {
@@ -418,7 +422,7 @@ struct tsv_ctx {
     unsigned cg_grid() const { return std::min<unsigned>(vec_grid(), static_cast<unsigned>(sm_count) * 8u); }
 
     void launch_scatter(const double *v, int mode) {
-        scatter_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), slots.ptr, cmask.ptr, v,
+        scatter_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), static_cast<int>(n / 3), slots.ptr, cmask.ptr, v,
                                                                     X.ptr, mode);
         ++launches;
         CK(cudaGetLastError());
@@ -464,6 +468,7 @@ struct tsv_ctx {
         CgParams q{};
         q.st = state.ptr;
         q.n_nodes = static_cast<int>(nodes);
+        q.nn = static_cast<int>(n / 3);
         q.slots = slots.ptr;
         q.cmask = cmask.ptr;
         q.b = b.ptr;
@@ -877,15 +882,19 @@ int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
         const size_t ldk = round_up(n, kKC);
         {
             std::vector<double> kp(round_up(n, kBN) * ldk, 0.0);
+            // component-major permutation a = 3 rank + c -> c nn + rank on both sides
+            const size_t nn = n / 3;
             for (size_t a = 0; a < n; ++a)
-                for (size_t k = 0; k < n; ++k) kp[a * ldk + k] = d->a_element[a * n + k];
+                for (size_t k = 0; k < n; ++k) kp[pidx(a, nn) * ldk + pidx(k, nn)] = d->a_element[a * n + k];
             m.d_k.upload(kp.data(), kp.size(), ctx->stream);
             CK(cudaStreamSynchronize(ctx->stream));
         }
         {
             const size_t rows = round_up(n_fine, kBN);
             std::vector<double> pp(rows * ldk, 0.0);
-            for (size_t f = 0; f < n_fine; ++f) std::memcpy(pp.data() + f * ldk, d->basis + f * n, n * sizeof(double));
+            const size_t nn = n / 3;
+            for (size_t f = 0; f < n_fine; ++f)
+                for (size_t a = 0; a < n; ++a) pp[f * ldk + pidx(a, nn)] = d->basis[f * n + a];
             m.d_phi.upload(pp.data(), pp.size(), ctx->stream);
             std::vector<double> ut(rows, 0.0);
             std::memcpy(ut.data(), d->thermal, n_fine * sizeof(double));
@@ -1016,7 +1025,8 @@ int tsv_apply(tsv_ctx *ctx, const double *xin, double *yout) {
         ctx->launch_scatter(ctx->r.ptr, 0);
         ctx->launch_k1(nullptr);
         gather_vec_kernel<<<ctx->vec_grid(), kVecThreads, 0, ctx->stream>>>(
-            static_cast<int>(ctx->nodes), ctx->slots.ptr, ctx->cmask.ptr, ctx->Y.ptr, ctx->r.ptr, ctx->ap.ptr, 0);
+            static_cast<int>(ctx->nodes), static_cast<int>(ctx->n / 3), ctx->slots.ptr, ctx->cmask.ptr, ctx->Y.ptr, ctx->r.ptr,
+            ctx->ap.ptr, 0);
         ++ctx->launches;
         CK(cudaGetLastError());
         std::vector<double> yi(ctx->N);

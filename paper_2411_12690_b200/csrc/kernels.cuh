@@ -233,17 +233,23 @@ struct CgState {
     unsigned ticket_a, ticket_b;
 };
 
+// Device vectors are structure-of-arrays per component: DoF (node, c) of
+// the internal node order lives at c * n_nodes + node. Block panels (X, Y)
+// are component-major within a row: local DoF (rank, c) at c * nn + rank,
+// with K_r / Phi permuted to match at upload. slots[node] holds the row
+// offsets row * ldk + rank of the node's 1, 2 or 4 block copies.
 struct CgParams {
     CgState *st;
     int n_nodes;
-    const int *slots;   // [node][4] offsets into X / Y (-1 = none), ascending block order
-    const uint8_t *cmask;  // [dof] constrained
+    int nn;             // surface nodes per block (panel component stride)
+    const int *slots;   // [node][4] panel offsets (-1 = none), ascending block order
+    const uint8_t *cmask;  // [3][node] constrained
     const double *b;
     double *x, *r, *p, *ap;
     const double *Y;    // block products
     double *X;          // block-major operand panel
     int precond;        // 0 none, 1 diagonal, 2 3x3 node blocks
-    const double *pre;  // inv_diag [dof] or inverse node blocks [node][9]
+    const double *pre;  // inv_diag [3][node] or inverse node blocks [9][node]
     double *partial;    // [grid][2]
 };
 
@@ -259,6 +265,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *sh /* [32*NV]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+    __syncthreads();
     if (lane == 0)
 #pragma unroll
         for (int i = 0; i < NV; ++i) sh[warp * NV + i] = v[i];
@@ -286,12 +293,15 @@ __device__ __forceinline__ void grid_sum(const double *partial, int nblocks, dou
     block_sum<NV>(out, sh);
 }
 
-__device__ __forceinline__ void precond_node(int kind, const double *pre, int node, const double r[3], double z[3]) {
+__device__ __forceinline__ void precond_node(int kind, const double *pre, int node, int n_nodes, const double r[3],
+                                             double z[3]) {
     if (kind == 1) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) z[c] = pre[3 * node + c] * r[c];
+        for (int c = 0; c < 3; ++c) z[c] = pre[c * n_nodes + node] * r[c];
     } else if (kind == 2) {
-        const double *m = pre + 9 * static_cast<long long>(node);
+        double m[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) m[k] = pre[static_cast<long long>(k) * n_nodes + node];
         z[0] = m[0] * r[0] + m[1] * r[1] + m[2] * r[2];
         z[1] = m[3] * r[0] + m[4] * r[1] + m[5] * r[2];
         z[2] = m[6] * r[0] + m[7] * r[1] + m[8] * r[2];
@@ -323,21 +333,23 @@ __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int yx = st->y_holds_x;
+    const int N = q.n_nodes;
     double part[1] = {0.0};
-    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < q.n_nodes; node += gridDim.x * blockDim.x) {
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const long long dof = 3LL * node + c;
+            const long long dof = static_cast<long long>(c) * N + node;
+            const int co = c * q.nn;
             double acc;
             if (q.cmask[dof]) {
                 acc = yx ? q.x[dof] : q.p[dof];  // unit row of the lifted matrix
             } else {
                 acc = 0.0;
-                if (s.x >= 0) acc += q.Y[s.x + c];
-                if (s.y >= 0) acc += q.Y[s.y + c];
-                if (s.z >= 0) acc += q.Y[s.z + c];
-                if (s.w >= 0) acc += q.Y[s.w + c];
+                if (s.x >= 0) acc += q.Y[s.x + co];
+                if (s.y >= 0) acc += q.Y[s.y + co];
+                if (s.z >= 0) acc += q.Y[s.z + co];
+                if (s.w >= 0) acc += q.Y[s.w + co];
             }
             if (!yx) {
                 q.ap[dof] = acc;
@@ -385,12 +397,13 @@ __global__ void __launch_bounds__(256) cg_update_kernel(CgParams q) {
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int phase = st->phase;
     const double alpha = st->alpha;
+    const int N = q.n_nodes;
     double part[2] = {0.0, 0.0};
-    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < q.n_nodes; node += gridDim.x * blockDim.x) {
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         double r3[3], z3[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const long long dof = 3LL * node + c;
+            const long long dof = static_cast<long long>(c) * N + node;
             double rv;
             if (phase == PH_NORMAL) {
                 q.x[dof] += alpha * q.p[dof];
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(CgParams q) {
             }
             r3[c] = rv;
         }
-        precond_node(q.precond, q.pre, node, r3, z3);
+        precond_node(q.precond, q.pre, node, N, r3, z3);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             part[0] += r3[c] * z3[c];
@@ -471,26 +484,25 @@ __global__ void __launch_bounds__(256) cg_scatter_kernel(CgParams q) {
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int p_assign = st->p_assign, yx = st->y_holds_x;
     const double beta = st->beta;
-    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < q.n_nodes; node += gridDim.x * blockDim.x) {
-        double r3[3], z3[3], v[3];
+    const int N = q.n_nodes;
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+        double r3[3], z3[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) r3[c] = q.r[3LL * node + c];
-        precond_node(q.precond, q.pre, node, r3, z3);
+        for (int c = 0; c < 3; ++c) r3[c] = q.r[static_cast<long long>(c) * N + node];
+        precond_node(q.precond, q.pre, node, N, r3, z3);
+        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const long long dof = 3LL * node + c;
+            const long long dof = static_cast<long long>(c) * N + node;
             const double pn = p_assign ? z3[c] : z3[c] + beta * q.p[dof];
             q.p[dof] = pn;
-            v[c] = yx ? q.x[dof] : pn;
-        }
-        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
-        const int sl[4] = {s.x, s.y, s.z, s.w};
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            if (q.cmask[3LL * node + c]) continue;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (sl[k] >= 0) q.X[sl[k] + c] = v[c];
+            if (q.cmask[dof]) continue;
+            const double v = yx ? q.x[dof] : pn;
+            const int co = c * q.nn;
+            if (s.x >= 0) q.X[s.x + co] = v;
+            if (s.y >= 0) q.X[s.y + co] = v;
+            if (s.z >= 0) q.X[s.z + co] = v;
+            if (s.w >= 0) q.X[s.w + co] = v;
         }
     }
 }
@@ -499,7 +511,7 @@ __global__ void __launch_bounds__(256) cg_scatter_kernel(CgParams q) {
 // mode 0: X[slot] = v (free DoFs only, constrained slots zeroed)
 // mode 1: X[slot] = v for every DoF (recovery uses u at all DoFs)
 // mode 2: X[slot] = v on constrained DoFs only, 0 elsewhere (A_fc g)
-__global__ void scatter_vec_kernel(int n_nodes, const int *slots, const uint8_t *cmask, const double *v,
+__global__ void scatter_vec_kernel(int n_nodes, int nn, const int *slots, const uint8_t *cmask, const double *v,
                                    double *X, int mode) {
     const int node = blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= n_nodes) return;
@@ -507,30 +519,31 @@ __global__ void scatter_vec_kernel(int n_nodes, const int *slots, const uint8_t 
     const int sl[4] = {s.x, s.y, s.z, s.w};
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const long long dof = 3LL * node + c;
+        const long long dof = static_cast<long long>(c) * n_nodes + node;
         const bool cm = cmask[dof] != 0;
         double val = v[dof];
         if ((mode == 0 && cm) || (mode == 2 && !cm)) val = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (sl[k] >= 0) X[sl[k] + c] = val;
+            if (sl[k] >= 0) X[sl[k] + c * nn] = val;
     }
 }
 
 // y = Mf o sum(Y) + Mc o x  (mode 0), or b_f -= sum(Y), b_c = g (mode 1).
-__global__ void gather_vec_kernel(int n_nodes, const int *slots, const uint8_t *cmask, const double *Y,
+__global__ void gather_vec_kernel(int n_nodes, int nn, const int *slots, const uint8_t *cmask, const double *Y,
                                   const double *x, double *y, int mode) {
     const int node = blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= n_nodes) return;
     const int4 s = reinterpret_cast<const int4 *>(slots)[node];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const long long dof = 3LL * node + c;
+        const long long dof = static_cast<long long>(c) * n_nodes + node;
+        const int co = c * nn;
         double acc = 0.0;
-        if (s.x >= 0) acc += Y[s.x + c];
-        if (s.y >= 0) acc += Y[s.y + c];
-        if (s.z >= 0) acc += Y[s.z + c];
-        if (s.w >= 0) acc += Y[s.w + c];
+        if (s.x >= 0) acc += Y[s.x + co];
+        if (s.y >= 0) acc += Y[s.y + co];
+        if (s.z >= 0) acc += Y[s.z + co];
+        if (s.w >= 0) acc += Y[s.w + co];
         if (mode == 0) {
             y[dof] = cmask[dof] ? x[dof] : acc;
         } else {
