@@ -84,6 +84,7 @@ typedef struct { /* GlobalSolution (global.hpp:91-96) + device timings */
     int direct_fallback;      /* always 0: no CPU fallback on the GPU path */
     int best_iterations;      /* on TSV_ENOCONV: iteration of the returned best iterate */
     double solve_ms;          /* device time of the solve, CUDA events on the context stream */
+    double loop_ms;           /* of which the iteration loop (excludes the best-iterate replay) */
     uint64_t kernel_launches; /* kernels launched by this call */
 } tsv_solve_info;
 

@@ -115,6 +115,7 @@ class GlobalSolution:
     best_iterations: int = 0
     solve_ms: float = 0.0
     kernel_launches: int = 0
+    loop_ms: float = 0.0
 
 
 @dataclass
@@ -252,7 +253,7 @@ class GpuGlobalStage:
         u = np.empty(self.index().dof_count) if copy_out else None
         rc = self._L.tsv_solve(self._h, C.byref(o), _p(u), C.byref(info))
         sol = GlobalSolution(u, info.iterations, info.relative_residual, bool(info.direct_fallback),
-                             info.best_iterations, info.solve_ms, info.kernel_launches)
+                             info.best_iterations, info.solve_ms, info.kernel_launches, info.loop_ms)
         if rc == TSV_ENOCONV:
             raise NoConvergence(self._L.tsv_last_error(self._h).decode(), sol)
         self._check(rc, "solve_global")

@@ -515,6 +515,10 @@ struct tsv_ctx {
         const uint64_t l0 = launches;
         CK(cudaEventRecord(ev0, stream));
         CgState st = run_cg(o.tolerance, o.max_iterations);
+        float loop_ms = 0.f;
+        CK(cudaEventRecord(ev1, stream));
+        CK(cudaEventSynchronize(ev1));
+        CK(cudaEventElapsedTime(&loop_ms, ev0, ev1));
         int status = TSV_OK;
         int best_it = st.it;
         double relres = st.norm_b > 0.0 ? st.res / st.norm_b : 0.0;
@@ -553,6 +557,7 @@ struct tsv_ctx {
             info->direct_fallback = 0;
             info->best_iterations = best_it;
             info->solve_ms = ms;
+            info->loop_ms = loop_ms;
             info->kernel_launches = launches - l0;
         }
         if (status == TSV_ENOCONV) {

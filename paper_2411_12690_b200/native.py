@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtsv_b200.so")
+LIB_PATH = os.environ.get("TSV_B200_LIB") or os.path.join(HERE, "_lib", "libtsv_b200.so")
 
 TSV_OK, TSV_EINVAL, TSV_ENOCONV, TSV_EBREAKDOWN, TSV_ECUDA, TSV_ENOMEM, TSV_ESTATE = range(7)
 
@@ -45,7 +45,8 @@ class IterOptionsC(C.Structure):
 
 class SolveInfo(C.Structure):
     _fields_ = [("iterations", C.c_int), ("relative_residual", C.c_double), ("direct_fallback", C.c_int),
-                ("best_iterations", C.c_int), ("solve_ms", C.c_double), ("kernel_launches", C.c_uint64)]
+                ("best_iterations", C.c_int), ("solve_ms", C.c_double), ("loop_ms", C.c_double),
+                ("kernel_launches", C.c_uint64)]
 
 
 class LocalDesc(C.Structure):
