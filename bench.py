@@ -212,26 +212,11 @@ def run_reference(args, cfg, rank, world):
 def run_ours(args, cfg, rank, local_rank, world):
     from paper_2411_12690_b200 import native
     from paper_2411_12690_b200.api import ArrayLayout, IterOptions
+    from paper_2411_12690_b200.replicas import Ranks, aggregate_throughput
     L = native.load()
     dev = local_rank
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(dev)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    ranks = Ranks(device=dev)  # NCCL barrier / max over ranks for N replicas
+    barrier, max_over_ranks = ranks.barrier, ranks.max
 
     rom_tsv, rom_dum, t_rom = build_inputs(cfg, dev)
     g, layout = make_stage(cfg, rom_tsv, rom_dum, dev)
@@ -259,7 +244,7 @@ def run_ours(args, cfg, rank, local_rank, world):
     barrier()
     launches = g.timing().kernel_launches - launches0
     ms_step = max_over_ranks(sum(dev_ms) / len(dev_ms))
-    value = world * cfg.B / (ms_step / 1e3)
+    value = aggregate_throughput(cfg.B, world, ms_step)
     solve_ms, recover_ms = tm.solve_ms, tm.recover_ms
 
     # dominant kernel (K1 operator apply) on its own stream, CUDA events
@@ -299,7 +284,7 @@ def run_ours(args, cfg, rank, local_rank, world):
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2: {out_bytes / 1e9:.1f} GB stress output + {ix.dof_count * 8 * 6 / 1e6:.0f} MB vectors per step"},
         "roofline": {"bound": "tensor", "achieved": k1_flops / (k1_ms * 1e-3) / 1e12, "peak": dmma_peak,
-                     "unit": "TFLOP/s", "frac": k1_flops / (k1_ms * 1e-3) / 1e12 / dmma_peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": k1_flops / (k1_ms * 1e-3) / 1e12 / dmma_peak, "traffic": k1_traffic(cfg),
                      "kernel": "gemm_nt_f64 (K1 operator apply, 2n^2 B FLOP per launch)",
                      "peak_source": "measured live: register-only DMMA.8x8x4 loop (tsv_fp64_peak); MEASURED_PEAKS.json has no FP64 entry"},
         "end_to_end_roofline": {"t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_step,
@@ -318,9 +303,17 @@ def run_ours(args, cfg, rank, local_rank, world):
     if rank == 0:
         print(json.dumps(line), flush=True)
     g.close()
-    if dist is not None:
-        dist.destroy_process_group()
+    ranks.close()
     return 0
+
+
+def k1_traffic(cfg):
+    """DRAM bytes per K1 launch from the committed ncu capture (profiles/k1_traffic.json), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))[cfg.name]
+        return t["dram_read_bytes"] + t["dram_write_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def ctypes_peak(L, dev):

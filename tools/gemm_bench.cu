@@ -42,14 +42,11 @@ int main(int argc, char **argv) {
     cudaMemset(B, 0, (size_t)Npad * K * 8);
     cudaMemcpy(B, h.data(), (size_t)N * K * 8, cudaMemcpyHostToDevice);
     run<GemmCfg<128, 64, 2, 2, 16, 3, 2>>("128x64_w2x2_kc16_s3", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<128, 64, 2, 2, 32, 2, 2>>("128x64_w2x2_kc32_s2", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<128, 64, 2, 2, 16, 4, 1>>("128x64_w2x2_kc16_s4_1cta", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<64, 64, 2, 2, 16, 4, 3>>("64x64_w2x2_kc16_s4", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<64, 64, 2, 2, 32, 3, 3>>("64x64_w2x2_kc32_s3", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<128, 128, 2, 4, 16, 3, 1>>("128x128_w2x4_kc16_s3", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<256, 64, 4, 2, 16, 3, 1>>("256x64_w4x2_kc16_s3", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<128, 32, 4, 1, 16, 4, 2>>("128x32_w4x1_kc16_s4", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<64, 128, 1, 4, 16, 3, 2>>("64x128_w1x4_kc16_s3", M, N, K, A, B, C, ctr, sms);
-    run<GemmCfg<128, 64, 4, 2, 16, 3, 1>>("128x64_w4x2_kc16_s3", M, N, K, A, B, C, ctr, sms);
+    run<GemmCfg<128, 64, 2, 2, 16, 2, 3>>("128x64_w2x2_kc16_s2_3cta", M, N, K, A, B, C, ctr, sms);
+    run<GemmCfg<128, 64, 2, 2, 8, 4, 3>>("128x64_w2x2_kc8_s4_3cta", M, N, K, A, B, C, ctr, sms);
+    run<GemmCfg<64, 128, 2, 2, 16, 3, 2>>("64x128_w2x2_kc16_s3", M, N, K, A, B, C, ctr, sms);
+    run<GemmCfg<128, 64, 2, 2, 8, 6, 2>>("128x64_w2x2_kc8_s6", M, N, K, A, B, C, ctr, sms);
+    run<GemmCfg<128, 96, 2, 2, 16, 3, 2>>("128x96_w2x2_kc16_s3", M, N, K, A, B, C, ctr, sms);
+    run<GemmCfg<96, 64, 2, 2, 16, 3, 2>>("96x64_w2x2_kc16_s3", M, N, K, A, B, C, ctr, sms);
     return 0;
 }
