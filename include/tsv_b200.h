@@ -157,6 +157,12 @@ int tsv_recover(tsv_ctx *ctx, int points, uint64_t cell_begin, uint64_t cell_end
 int tsv_recover_resident(tsv_ctx *ctx, int points);
 int tsv_copy_stress(tsv_ctx *ctx, uint64_t cell_begin, uint64_t cell_end, double *out);
 
+/* cutplane_von_mises (global_stage.cpp:245-274): von Mises at res x res
+ * cell-centred samples of z = h/2 in every block, the containing element
+ * chosen with locate_axis_cell's lower-cell tie rule (mesh.cpp:97-104).
+ * out = StressGrid::values, [((row*cols + col)*res + py)*res + px]. */
+int tsv_cutplane(tsv_ctx *ctx, uint32_t res, double *out);
+
 /* Reconstructed fine displacement of one cell (reconstruct_block_field). */
 int tsv_block_field(tsv_ctx *ctx, uint64_t cell, double *out /* n_fine */);
 

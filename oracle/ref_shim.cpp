@@ -450,3 +450,18 @@ int64_t ref_index(uint32_t rows, uint32_t cols, uint32_t q, uint32_t *dof_map) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+/// StressGrid::save_csv (stress_grid.cpp:36-50) of given values, for the
+/// byte-format check of the product's CSV writer.
+int ref_stress_grid_save_csv(const double *values, uint32_t rows, uint32_t cols, uint32_t res, double pitch,
+                             const char *path) {
+    return guarded([&] {
+        StressGrid g = StressGrid::make(rows, cols, res, pitch);
+        std::memcpy(g.values.data(), values, g.values.size() * sizeof(double));
+        g.save_csv(path);
+    });
+}
+
+}  // extern "C"

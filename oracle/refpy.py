@@ -247,3 +247,12 @@ def index_dof_map(rows, cols, q):
     out = np.empty((rows * cols, n), np.uint32)
     L.ref_index(rows, cols, q, _ptr(out))
     return nd, out
+
+
+def stress_grid_save_csv(values, rows, cols, res, pitch, path):
+    """The reference's StressGrid::save_csv on given values."""
+    L = lib()
+    L.ref_stress_grid_save_csv.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_double, C.c_char_p]
+    v = np.ascontiguousarray(values, np.float64)
+    if L.ref_stress_grid_save_csv(_ptr(v), rows, cols, res, pitch, path.encode()) != 0:
+        raise RefError(_err())

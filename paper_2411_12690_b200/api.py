@@ -282,6 +282,13 @@ class GpuGlobalStage:
         self._check(self._L.tsv_copy_stress(self._h, cell_begin, cell_end, _p(out)), "copy_stress")
         return out
 
+    def cutplane_von_mises(self, res: int = 100) -> np.ndarray:
+        """cutplane_von_mises (global_stage.cpp:245-274) on the GPU:
+        StressGrid values [cell, py, px] at z = h/2."""
+        out = np.empty((self.layout.cell_count, res, res))
+        self._check(self._L.tsv_cutplane(self._h, res, _p(out)), "cutplane_von_mises")
+        return out
+
     def block_field(self, cell: int):
         r = self.roms[0] or self.roms[1]
         out = np.empty(r.fine_dofs)
@@ -423,3 +430,21 @@ def load_rom(path: str) -> ReducedOrderModel:
     return ReducedOrderModel(q=tuple(q), geometry=tuple(geom), grid=tuple(grid), materials=mats, a_element=K,
                              b_element=b, basis=basis, thermal=thermal, element_material=None, fingerprint=fp,
                              kind=kind)
+
+
+def save_stress_grid_csv(values, rows: int, cols: int, pitch: float, path: str) -> None:
+    """StressGrid::save_csv (stress_grid.cpp:36-50): the reference's CSV,
+    block_row,block_col,px,py,x,y,von_mises with %.17g numbers."""
+    v = np.asarray(values, np.float64).reshape(rows, cols, -1)
+    res = int(round(np.sqrt(v.shape[2])))
+    v = v.reshape(rows, cols, res, res)
+    local = [(q + 0.5) * pitch / res for q in range(res)]
+    with open(path, "w", newline="\n") as f:
+        f.write("block_row,block_col,px,py,x,y,von_mises\n")
+        for r in range(rows):
+            for c in range(cols):
+                for py in range(res):
+                    y = r * pitch + local[py]
+                    for px in range(res):
+                        x = c * pitch + local[px]
+                        f.write("%d,%d,%d,%d,%.17g,%.17g,%.17g\n" % (r, c, px, py, x, y, v[r, c, py, px]))

@@ -95,7 +95,7 @@ struct RomHost {
     std::vector<double> k_r, b_el, u_t;  // host copies used for assembly of b / preconditioners
     size_t n = 0, n_fine = 0, cells[3] = {0, 0, 0};
     uint8_t fingerprint[32] = {};
-    DevBuf<double> d_k, d_phi, d_ut, d_hinv;
+    DevBuf<double> d_k, d_phi, d_ut, d_hinv, d_grid[3];
     DevBuf<uint8_t> d_em;
 };
 
@@ -616,6 +616,8 @@ struct tsv_ctx {
     }
 
     // Recover cells [c0, c1) into device buffer `out` (cells-relative).
+    // Recover cells [c0, c1) into device buffer `out` (cells-relative):
+    // points = 8 / 1 -> stress_kernel; points = -res -> cut-plane samples.
     void recover_range(int points, size_t c0, size_t c1, double *out) {
         const RomHost &m = rom[0].set ? rom[0] : rom[1];
         const size_t ldu = round_up(m.n_fine, 8);
@@ -671,10 +673,37 @@ struct tsv_ctx {
             gp.done = nullptr;
             gp.tile_counter = tile_counter.ptr;
             gemm_nt_f64<K6Cfg><<<k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
-            sp.U = U.ptr;
-            sp.j0 = static_cast<int>(t * kBM);
-            dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>(m.cells[2]));
-            stress_kernel<<<grid, 256, smem, stream>>>(sp);
+            if (points > 0) {
+                sp.U = U.ptr;
+                sp.j0 = static_cast<int>(t * kBM);
+                dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>(m.cells[2]));
+                stress_kernel<<<grid, 256, smem, stream>>>(sp);
+            } else {
+                const int res = -points;
+                CutParams cp{};
+                cp.U = U.ptr;
+                cp.ldu = static_cast<long long>(ldu);
+                cp.j0 = static_cast<int>(t * kBM);
+                cp.row_cell = row_cell_d.ptr;
+                cp.row_kind = row_kind_d.ptr;
+                cp.row_dt = row_dt_d.ptr;
+                for (int kk = 0; kk < 2; ++kk) {
+                    const RomHost &mk2 = rom[kk].set ? rom[kk] : m;
+                    for (int a = 0; a < 3; ++a) cp.grid[kk][a] = mk2.d_grid[a].ptr;
+                    cp.elem_mat[kk] = mk2.d_em.ptr;
+                    for (int a = 0; a < 3; ++a)
+                        for (int b2 = 0; b2 < 3; ++b2) cp.lame[kk][a][b2] = mk2.lame[a][b2];
+                }
+                for (int a = 0; a < 3; ++a) cp.len[a] = static_cast<int>(m.grid[a].size());
+                cp.res = res;
+                cp.pitch = layout.pitch;
+                cp.z_mid = 0.5 * layout.height;
+                cp.out = out;
+                cp.out_cell0 = static_cast<long long>(c0);
+                cp.out_cells = static_cast<long long>(c1 - c0);
+                dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>((res * res + 255) / 256));
+                cutplane_kernel<<<grid, 256, 0, stream>>>(cp);
+            }
             launches += 2;
             CK(cudaGetLastError());
             t = t1;
@@ -910,6 +939,7 @@ int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
         for (int a = 0; a < 3; ++a)
             for (size_t i = 0; i < m.cells[a]; ++i) hinv.push_back(1.0 / (m.grid[a][i + 1] - m.grid[a][i]));
         m.d_hinv.upload(hinv.data(), hinv.size(), ctx->stream);
+        for (int a = 0; a < 3; ++a) m.d_grid[a].upload(m.grid[a].data(), m.grid[a].size(), ctx->stream);
         m.d_em.upload(m.elem_mat.data(), E, ctx->stream);
         CK(cudaStreamSynchronize(ctx->stream));
         m.set = true;
@@ -1115,6 +1145,32 @@ int tsv_copy_stress(tsv_ctx *ctx, uint64_t c0, uint64_t c1, double *out) {
         const size_t per_cell = ctx->elems() * static_cast<size_t>(ctx->stress_points) * 7;
         CK(cudaMemcpy(out, ctx->stress.ptr + c0 * per_cell, (c1 - c0) * per_cell * sizeof(double),
                       cudaMemcpyDeviceToHost));
+        return TSV_OK;
+    });
+}
+
+int tsv_cutplane(tsv_ctx *ctx, uint32_t res, double *out) {
+    return guarded(ctx, [&] {
+        cudaSetDevice(ctx->device);
+        ctx->check_recovery(8);
+        if (res < 1) throw StatusError(TSV_EINVAL, "StressGrid: rows, cols, res must be >= 1");
+        const size_t per_cell = static_cast<size_t>(res) * res;
+        const size_t max_cells = std::max<size_t>(1, (size_t(1) << 30) / (per_cell * sizeof(double)));
+        DevBuf<double> dout;
+        CK(cudaEventRecord(ctx->ev0, ctx->stream));
+        for (size_t a = 0; a < ctx->B; a += max_cells) {
+            const size_t b2 = std::min<size_t>(ctx->B, a + max_cells);
+            dout.alloc((b2 - a) * per_cell);
+            ctx->recover_range(-static_cast<int>(res), a, b2, dout.ptr);
+            CK(cudaMemcpyAsync(out + a * per_cell, dout.ptr, (b2 - a) * per_cell * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        CK(cudaEventRecord(ctx->ev1, ctx->stream));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+        ctx->last_recover_ms = ms;
         return TSV_OK;
     });
 }

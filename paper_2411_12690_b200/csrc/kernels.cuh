@@ -643,6 +643,99 @@ __global__ void stress_kernel(StressParams sp) {
     }
 }
 
+// ------------------------------------------------------------- cut plane
+// cutplane_von_mises (global_stage.cpp:245-274): von Mises at res x res
+// cell-centred samples of the plane z = h/2 of every block
+// (StressGrid::local_coord, stress_grid.cpp:32-34), the containing element
+// found with the reference's tie rule (locate_axis_cell, mesh.cpp:97-104:
+// a point on a grid plane belongs to the lower cell).
+struct CutParams {
+    const double *U;
+    long long ldu;
+    int j0;
+    const int *row_cell;
+    const uint8_t *row_kind;
+    const double *row_dt;
+    const double *grid[2][3];  // [kind][axis] grid lines
+    int len[3];                // grid line counts
+    const uint8_t *elem_mat[2];
+    double lame[2][3][3];
+    int res;
+    double pitch, z_mid;
+    double *out;               // StressGrid::values
+    long long out_cell0, out_cells;
+};
+
+__device__ __forceinline__ int locate_axis_cell(const double *axis, int len, double v) {
+    int lo = 0, hi = len;  // upper_bound: first index with axis[idx] > v
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (axis[mid] <= v) lo = mid + 1;
+        else hi = mid;
+    }
+    int k = lo == 0 ? 0 : lo - 1;  // axis[k] <= v
+    if (k > 0 && axis[k] == v) return k - 1;
+    return min(k, len - 2);
+}
+
+__global__ void cutplane_kernel(CutParams cp) {
+    const int jr = blockIdx.x;
+    const int j = cp.j0 + jr;
+    const int cell = cp.row_cell[j];
+    if (cell < 0) return;
+    const long long oc = cell - cp.out_cell0;
+    if (oc < 0 || oc >= cp.out_cells) return;
+    const int t = blockIdx.y * blockDim.x + threadIdx.x;
+    if (t >= cp.res * cp.res) return;
+    const int py = t / cp.res, px = t % cp.res;
+    const int kind = cp.row_kind[j];
+    const double *gx = cp.grid[kind][0], *gy = cp.grid[kind][1], *gz = cp.grid[kind][2];
+    const double x = (static_cast<double>(px) + 0.5) * cp.pitch / static_cast<double>(cp.res);
+    const double y = (static_cast<double>(py) + 0.5) * cp.pitch / static_cast<double>(cp.res);
+    const double z = cp.z_mid;
+    const int i = locate_axis_cell(gx, cp.len[0], x);
+    const int jj = locate_axis_cell(gy, cp.len[1], y);
+    const int k = locate_axis_cell(gz, cp.len[2], z);
+    const double x0 = gx[i], x1 = gx[i + 1], y0 = gy[jj], y1 = gy[jj + 1], z0 = gz[k], z1 = gz[k + 1];
+    const double xi = 2.0 * (x - x0) / (x1 - x0) - 1.0;  // fem.cpp:271-273
+    const double eta = 2.0 * (y - y0) / (y1 - y0) - 1.0;
+    const double zeta = 2.0 * (z - z0) / (z1 - z0) - 1.0;
+    const double hxi = 1.0 / (x1 - x0), hyi = 1.0 / (y1 - y0), hzi = 1.0 / (z1 - z0);
+    const int nx = cp.len[0], ny = cp.len[1];
+    const double *U = cp.U + static_cast<long long>(jr) * cp.ldu;
+    double du[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const int di = (a == 1 || a == 2 || a == 5 || a == 6);
+        const int dj = (a == 2 || a == 3 || a == 6 || a == 7);
+        const int dk = a >= 4;
+        const double sx = di ? 1.0 : -1.0, sy = dj ? 1.0 : -1.0, sz = dk ? 1.0 : -1.0;
+        const double gxa = 0.25 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta) * hxi;
+        const double gya = 0.25 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta) * hyi;
+        const double gza = 0.25 * sz * (1.0 + sx * xi) * (1.0 + sy * eta) * hzi;
+        const double *ua = U + 3LL * (((k + dk) * ny + (jj + dj)) * nx + (i + di));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            du[c][0] += ua[c] * gxa;
+            du[c][1] += ua[c] * gya;
+            du[c][2] += ua[c] * gza;
+        }
+    }
+    const long long e = (static_cast<long long>(k) * (ny - 1) + jj) * (nx - 1) + i;
+    const int mat = cp.elem_mat[kind][e];
+    const double lambda = cp.lame[kind][mat][0], mu = cp.lame[kind][mat][1];
+    const double thermal = cp.lame[kind][mat][2] * cp.row_dt[j];
+    const double exx = du[0][0], eyy = du[1][1], ezz = du[2][2];
+    const double tr = exx + eyy + ezz;
+    const double sxx = lambda * tr + 2.0 * mu * exx - thermal;
+    const double syy = lambda * tr + 2.0 * mu * eyy - thermal;
+    const double szz = lambda * tr + 2.0 * mu * ezz - thermal;
+    const double sxy = mu * (du[0][1] + du[1][0]), syz = mu * (du[1][2] + du[2][1]), szx = mu * (du[2][0] + du[0][2]);
+    const double d1 = sxx - syy, d2 = syy - szz, d3 = szz - sxx;
+    const double vm2 = 0.5 * (d1 * d1 + d2 * d2 + d3 * d3) + 3.0 * (sxy * sxy + syz * syz + szx * szx);
+    cp.out[(oc * cp.res + py) * cp.res + px] = sqrt(fmax(vm2, 0.0));
+}
+
 // ------------------------------------------------------------ peaks
 __global__ void peak_dmma_kernel(double *sink, int iters) {
     double acc[8][2];

@@ -18,7 +18,7 @@ EXPORTS = [
     "tsv_ctx_create", "tsv_ctx_destroy", "tsv_last_error", "tsv_abi_version", "tsv_set_rom", "tsv_set_layout",
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
     "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_solve", "tsv_set_solution", "tsv_recover",
-    "tsv_recover_resident", "tsv_copy_stress", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
+    "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
     "tsv_rom_dims", "tsv_build_rom", "tsv_host_register", "tsv_host_unregister", "tsv_fp64_peak",
 ]
 
@@ -101,6 +101,7 @@ def load(path: str = LIB_PATH):
         "tsv_recover": (i, [vp, i, u64, u64, vp]),
         "tsv_recover_resident": (i, [vp, i]),
         "tsv_copy_stress": (i, [vp, u64, u64, vp]),
+        "tsv_cutplane": (i, [vp, u32, vp]),
         "tsv_block_field": (i, [vp, u64, vp]),
         "tsv_profile_apply": (i, [vp, i, P(d)]),
         "tsv_get_timing": (i, [vp, P(Timing)]),
