@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -143,6 +144,10 @@ struct tsv_ctx {
     int k1_grid = 0, k6_grid = 0;
     int k1s_grid = 0;
     bool k1_small = false;  // small arrays: 64 x 64 tiles keep every SM busy
+    bool k1_streamk = false;  // large arrays: stream-K balanced K1
+    bool sk_resident = false;
+    DevBuf<int> sk_start, sk_flag;
+    DevBuf<double> sk_work;
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
@@ -227,6 +232,7 @@ struct tsv_ctx {
 
         // Few 128 x 64 tiles (small arrays): switch K1 to 64 x 64 tiles.
         k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(k1_grid);  // fewer tiles than CTA slots
+        setup_streamk();
 
         // Block-major node renumbering + slot table.
         const size_t nn = nl.node_count();
@@ -285,6 +291,52 @@ struct tsv_ctx {
         set_bc_mask(std::vector<uint8_t>(N, 0), std::vector<double>(N, 0.0));
         bc_set = false;
         CK(cudaStreamSynchronize(s));
+    }
+
+    // Stream-K boundaries for K1: split the linear (tile, k-chunk) space into
+    // k1_grid ranges of equal DMMA work (a chunk of a tile costs its number
+    // of valid 8-column fragments). Requires >= one full tile per range.
+    void setup_streamk() {
+        k1_streamk = false;
+        if (k1_small || !sk_resident || getenv_flag("TSV_NO_STREAMK")) return;
+        const size_t nt = round_up(n, kBN) / kBN, T = m_tiles * nt, KC = ldk / kKC, G = static_cast<size_t>(k1_grid);
+        const size_t nf = (n + 7) / 8, fpt = kBN / 8;
+        std::vector<double> w(nt);
+        for (size_t t = 0; t < nt; ++t) w[t] = static_cast<double>(std::min(fpt, nf - t * fpt));
+        double per_m = 0.0;
+        for (double v : w) per_m += v;
+        const double C = per_m * static_cast<double>(m_tiles) * static_cast<double>(KC);
+        // Wave efficiency of the dynamic tile queue: work / (tile rounds x slots).
+        // Stream-K pays extra segment prologues and partial fix-ups, so it is
+        // used only when the queue would waste > 12% in its last wave
+        // (deterministic choice: results stay bitwise reproducible).
+        const double rounds = std::ceil(static_cast<double>(T) / static_cast<double>(G));
+        const double eff = (C / (static_cast<double>(KC) * static_cast<double>(fpt))) / (rounds * static_cast<double>(G));
+        if (eff > 0.88) return;
+        std::vector<int> start(G + 1, 0);
+        size_t it = 0;
+        double cum = 0.0;
+        for (size_t g = 1; g < G; ++g) {
+            const double target = C * static_cast<double>(g) / static_cast<double>(G);
+            while (it < T * KC && cum + w[(it / KC) % nt] <= target) {
+                cum += w[(it / KC) % nt];
+                ++it;
+            }
+            start[g] = static_cast<int>(it);
+        }
+        start[G] = static_cast<int>(T * KC);
+        for (size_t g = 0; g < G; ++g)
+            if (static_cast<size_t>(start[g + 1] - start[g]) < KC) return;  // a tile could span 3 CTAs
+        sk_start.upload(start.data(), start.size(), stream);
+        sk_flag.alloc(G);
+        CK(cudaMemsetAsync(sk_flag.ptr, 0, G * sizeof(int), stream));
+        sk_work.alloc(G * static_cast<size_t>(K1Cfg::FM * K1Cfg::FN * 2 * K1Cfg::THREADS));
+        k1_streamk = true;
+    }
+
+    static bool getenv_flag(const char *name) {
+        const char *v = std::getenv(name);
+        return v && *v && *v != '0';
     }
 
     // ------------------------------------------------------------------ BC
@@ -457,6 +509,9 @@ struct tsv_ctx {
             gp.k_chunks = static_cast<int>(ldk / K1SmallCfg::KC);
             gp.tile_kind = tile_kind_small_d.ptr;
             gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+        } else if (k1_streamk) {
+            StreamK sk{sk_start.ptr, sk_work.ptr, sk_flag.ptr};
+            gemm_streamk_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp, sk);
         } else {
             gemm_nt_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp);
         }
@@ -825,6 +880,8 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1Cfg::SMEM)));
+        CK(cudaFuncSetAttribute(gemm_streamk_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K1Cfg::SMEM)));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1SmallCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1SmallCfg::SMEM)));
         int occ_s = 0;
@@ -834,6 +891,9 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_nt_f64<K1Cfg>, K1Cfg::THREADS, K1Cfg::SMEM));
         ctx->k1_grid = ctx->k6_grid = std::max(1, occ) * ctx->sm_count;
+        int occ_sk = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sk, gemm_streamk_f64<K1Cfg>, K1Cfg::THREADS, K1Cfg::SMEM));
+        ctx->sk_resident = occ_sk * ctx->sm_count >= ctx->k1_grid;  // stream-K waits need every CTA resident
         ctx->tile_counter.alloc(2);
         CK(cudaMemset(ctx->tile_counter.ptr, 0, 2 * sizeof(unsigned)));
         ctx->state.alloc(1);

@@ -118,6 +118,86 @@ __device__ __forceinline__ void mma_chunk_partial(double (&acc)[Cfg::FM][Cfg::FN
     }
 }
 
+// One tile segment: accumulate k-chunks [kc0, kc1) of tile (mt, nt).
+template <class Cfg>
+__device__ __forceinline__ void gemm_segment(const GemmParams &p, double *As, double *Bs, int mt, int nt, int kc0,
+                                             int kc1, int fn_lim, double (&acc)[Cfg::FM][Cfg::FN][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+    const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
+    const double *A0 = p.A + static_cast<long long>(mt) * Cfg::BM * p.lda;
+    const double *B0 = (kind ? p.Bt[1] : p.Bt[0]) + static_cast<long long>(nt) * Cfg::BN * p.ldb;
+#pragma unroll
+    for (int s = 0; s < Cfg::STAGES - 1; ++s) {
+        if (kc0 + s < kc1)
+            gemm_load_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, kc0 + s);
+        cp_async_commit();
+    }
+    for (int kc = kc0; kc < kc1; ++kc) {
+        const int i = kc - kc0;
+        cp_async_wait<Cfg::STAGES - 2>();
+        __syncthreads();
+        const int nk = kc + Cfg::STAGES - 1;
+        if (nk < kc1) {
+            const int st = (i + Cfg::STAGES - 1) % Cfg::STAGES;
+            gemm_load_stage<Cfg>(As + st * Cfg::A_STAGE, Bs + st * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, nk);
+        }
+        cp_async_commit();
+        const double *as = As + (i % Cfg::STAGES) * Cfg::A_STAGE + (wm * Cfg::TM + (lane >> 2)) * Cfg::SP + (lane & 3);
+        const double *bs = Bs + (i % Cfg::STAGES) * Cfg::B_STAGE + (wn * Cfg::TN + (lane >> 2)) * Cfg::SP + (lane & 3);
+        if (fn_lim == Cfg::FN)
+            mma_chunk<Cfg, Cfg::FN>(acc, as, bs);
+        else if (fn_lim > 0)
+            mma_chunk_partial<Cfg>(acc, as, bs, fn_lim);
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+}
+
+// Epilogue: lane holds C[row][col], C[row][col+1] (+ row_scale * col_bias).
+template <class Cfg>
+__device__ __forceinline__ void gemm_epilogue(const GemmParams &p, int mt, int nt,
+                                              const double (&acc)[Cfg::FM][Cfg::FN][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+    const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
+    const long long row0 = static_cast<long long>(mt) * Cfg::BM + wm * Cfg::TM + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < Cfg::FN; ++j) {
+        const int col = nt * Cfg::BN + wn * Cfg::TN + j * 8 + 2 * (lane & 3);
+        if (col >= p.n_store) continue;
+        double b0 = 0.0, b1 = 0.0;
+        const double *cb = kind ? p.col_bias[1] : p.col_bias[0];
+        if (p.row_scale) {
+            b0 = cb[col];
+            b1 = col + 1 < p.n_store ? cb[col + 1] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i) {
+            const long long row = row0 + i * 8;
+            double v0 = acc[i][j][0], v1 = acc[i][j][1];
+            if (p.row_scale) {
+                const double s = p.row_scale[row];
+                v0 += s * b0;
+                v1 += s * b1;
+            }
+            double *dst = p.C + row * p.ldc + col;
+            if (col + 1 < p.n_store) {
+                *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
+            } else {
+                dst[0] = v0;
+            }
+        }
+    }
+}
+
+template <class Cfg>
+__device__ __forceinline__ int gemm_fn_lim(const GemmParams &p, int nt) {
+    const int wn = (threadIdx.x >> 5) % Cfg::WN;
+    const int frag0 = nt * (Cfg::BN / 8) + wn * Cfg::FN;
+    return min(Cfg::FN, max(0, (p.n_valid + 7) / 8 - frag0));
+}
+
 // Persistent DMMA GEMM: grid = resident CTAs, tiles handed out by an atomic
 // counter (M tile major, N tile minor, so concurrently running CTAs share
 // the streamed A panel in L2).
@@ -127,10 +207,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
     __shared__ int s_tile;
     double *As = smem;
     double *Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
+    const int tid = threadIdx.x;
     const int total = p.m_tiles * p.n_tiles;
-    const int nf_valid = (p.n_valid + 7) / 8;
     const bool skip = p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0;
 
     while (!skip) {
@@ -140,72 +218,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
         __syncthreads();
         if (tile >= total) break;
         const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
-        const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
-        const double *A0 = p.A + static_cast<long long>(mt) * Cfg::BM * p.lda;
-        const double *B0 = (kind ? p.Bt[1] : p.Bt[0]) + static_cast<long long>(nt) * Cfg::BN * p.ldb;
-        const int frag0 = nt * (Cfg::BN / 8) + wn * Cfg::FN;
-        const int fn_lim = min(Cfg::FN, max(0, nf_valid - frag0));
-
         double acc[Cfg::FM][Cfg::FN][2];
 #pragma unroll
         for (int i = 0; i < Cfg::FM; ++i)
 #pragma unroll
             for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-#pragma unroll
-        for (int s = 0; s < Cfg::STAGES - 1; ++s) {
-            if (s < p.k_chunks)
-                gemm_load_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, s);
-            cp_async_commit();
-        }
-        for (int kc = 0; kc < p.k_chunks; ++kc) {
-            cp_async_wait<Cfg::STAGES - 2>();
-            __syncthreads();
-            const int nk = kc + Cfg::STAGES - 1;
-            if (nk < p.k_chunks) {
-                const int st = nk % Cfg::STAGES;
-                gemm_load_stage<Cfg>(As + st * Cfg::A_STAGE, Bs + st * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, nk);
-            }
-            cp_async_commit();
-            const double *as = As + (kc % Cfg::STAGES) * Cfg::A_STAGE + (wm * Cfg::TM + (lane >> 2)) * Cfg::SP + (lane & 3);
-            const double *bs = Bs + (kc % Cfg::STAGES) * Cfg::B_STAGE + (wn * Cfg::TN + (lane >> 2)) * Cfg::SP + (lane & 3);
-            if (fn_lim == Cfg::FN)
-                mma_chunk<Cfg, Cfg::FN>(acc, as, bs);
-            else if (fn_lim > 0)
-                mma_chunk_partial<Cfg>(acc, as, bs, fn_lim);
-        }
-        cp_async_wait<0>();
-        __syncthreads();
-
-        // Epilogue: lane holds C[row][col], C[row][col+1].
-        const long long row0 = static_cast<long long>(mt) * Cfg::BM + wm * Cfg::TM + (lane >> 2);
-#pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) {
-            const int col = nt * Cfg::BN + wn * Cfg::TN + j * 8 + 2 * (lane & 3);
-            if (col >= p.n_store) continue;
-            double b0 = 0.0, b1 = 0.0;
-            const double *cb = kind ? p.col_bias[1] : p.col_bias[0];
-            if (p.row_scale) {
-                b0 = cb[col];
-                b1 = col + 1 < p.n_store ? cb[col + 1] : 0.0;
-            }
-#pragma unroll
-            for (int i = 0; i < Cfg::FM; ++i) {
-                const long long row = row0 + i * 8;
-                double v0 = acc[i][j][0], v1 = acc[i][j][1];
-                if (p.row_scale) {
-                    const double s = p.row_scale[row];
-                    v0 += s * b0;
-                    v1 += s * b1;
-                }
-                double *dst = p.C + row * p.ldc + col;
-                if (col + 1 < p.n_store) {
-                    *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
-                } else {
-                    dst[0] = v0;
-                }
-            }
-        }
+        gemm_segment<Cfg>(p, As, Bs, mt, nt, 0, p.k_chunks, gemm_fn_lim<Cfg>(p, nt), acc);
+        gemm_epilogue<Cfg>(p, mt, nt, acc);
     }
     // The last CTA out resets the tile counter for the next launch.
     if (tid == 0) {
@@ -215,6 +234,79 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
             p.tile_counter[1] = 0u;
             __threadfence();
         }
+    }
+}
+
+// Stream-K DMMA GEMM: CTA g owns the linear (tile, k-chunk) iterations
+// [start[g], start[g+1]) (host-balanced by DMMA work), so every SM finishes
+// together instead of idling through a partial last wave. A tile split
+// between CTAs g and g+1 is completed by g (its k-chunks start at 0): g+1
+// computes the tail segment first, parks the partial accumulators in
+// work[g] and raises flag[g]; g adds them after its own segment, in that
+// fixed order, so results are bitwise reproducible. Requires every tile to
+// span at most two CTAs (host checks >= 2 tiles of work per CTA) and all
+// CTAs resident (grid = occupancy x SMs).
+struct StreamK {
+    const int *start;   // [grid + 1] linear iteration boundaries
+    double *work;       // [grid][FM*FN*2][THREADS]
+    int *flag;          // [grid], zero between launches
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_streamk_f64(GemmParams p, StreamK sk) {
+    extern __shared__ __align__(16) double smem[];
+    double *As = smem;
+    double *Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
+    constexpr int NACC = Cfg::FM * Cfg::FN * 2;
+    const int tid = threadIdx.x, g = blockIdx.x;
+    if (p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) return;
+    const int KC = p.k_chunks;
+    const int i0 = sk.start[g], i1 = sk.start[g + 1];
+    int it = i0;
+    while (it < i1) {
+        const int tile = it / KC, kc0 = it % KC;
+        const int kc1 = min(KC, kc0 + (i1 - it));
+        const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        gemm_segment<Cfg>(p, As, Bs, mt, nt, kc0, kc1, gemm_fn_lim<Cfg>(p, nt), acc);
+        if (kc0 > 0) {
+            // tail of a tile owned by CTA g-1: park the partial, raise the flag
+            double *w = sk.work + static_cast<long long>(g - 1) * NACC * Cfg::THREADS + tid;
+#pragma unroll
+            for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+                for (int j = 0; j < Cfg::FN; ++j) {
+                    w[((i * Cfg::FN + j) * 2 + 0) * Cfg::THREADS] = acc[i][j][0];
+                    w[((i * Cfg::FN + j) * 2 + 1) * Cfg::THREADS] = acc[i][j][1];
+                }
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) atomicExch(&sk.flag[g - 1], 1);
+        } else {
+            if (kc1 < KC) {
+                // head of a split tile: wait for CTA g+1's tail partial
+                if (tid == 0)
+                    while (atomicAdd(&sk.flag[g], 0) == 0) __nanosleep(64);
+                __syncthreads();
+                __threadfence();
+                const double *w = sk.work + static_cast<long long>(g) * NACC * Cfg::THREADS + tid;
+#pragma unroll
+                for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+                    for (int j = 0; j < Cfg::FN; ++j) {
+                        acc[i][j][0] += __ldcg(w + ((i * Cfg::FN + j) * 2 + 0) * Cfg::THREADS);
+                        acc[i][j][1] += __ldcg(w + ((i * Cfg::FN + j) * 2 + 1) * Cfg::THREADS);
+                    }
+                __syncthreads();
+                if (tid == 0) sk.flag[g] = 0;  // ready for the next launch
+            }
+            gemm_epilogue<Cfg>(p, mt, nt, acc);
+        }
+        it += kc1 - kc0;
     }
 }
 
