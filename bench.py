@@ -266,6 +266,7 @@ def run_ours(args, cfg, rank, local_rank, world):
     if rank == 0:
         os.makedirs(os.path.dirname(ITER_RECORD), exist_ok=True)
         rec = json.load(open(ITER_RECORD)) if os.path.exists(ITER_RECORD) else {}
+        rec = {k: v for k, v in rec.items() if not k.startswith("_")} | {k: v for k, v in rec.items() if k.startswith("_")}
         rec[cfg.name] = iters
         json.dump(rec, open(ITER_RECORD, "w"), indent=1, sort_keys=True)
 
