@@ -104,6 +104,13 @@ int tsv_abi_version(void);
  * element materials to HBM. */
 int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *rom);
 
+/* The reference's ".rom" files (MRST v1, rom.cpp:257-377) straight into a
+ * RomSet slot: magic/version/kind checks, SHA-256 header fingerprint,
+ * length validation, column-major basis. slot < 0 uses the file's kind. */
+int tsv_load_rom_file(tsv_ctx *ctx, int slot, const char *path, int *kind_out, char *err, size_t err_len);
+/* save_rom (rom.cpp:262-303) of a ROM given as a descriptor. */
+int tsv_save_rom_file(const tsv_rom_desc *rom, int kind, const char *path, char *err, size_t err_len);
+
 /* ArrayLayout (global.hpp:16-32) + RomSet::check_consistency (:52-80) +
  * index_global_nodes (global_stage.cpp:94-119): builds the global index,
  * the B x n dof map and the device-side gather/scatter tables. kinds may be

@@ -189,6 +189,16 @@ class GpuGlobalStage:
         self._check(self._L.tsv_set_rom(self._h, kind, C.byref(d)), "set_rom")
         self.roms[kind] = rom
 
+    def load_rom_file(self, path: str, slot: int = -1) -> int:
+        """Ingest a reference .rom file (MRST v1) natively into a RomSet slot
+        (slot -1 = the file's kind); returns the kind stored in the file."""
+        kind = C.c_int()
+        err = C.create_string_buffer(512)
+        rc = self._L.tsv_load_rom_file(self._h, slot, path.encode(), C.byref(kind), err, 512)
+        if rc != TSV_OK:
+            raise Error(f"load_rom: {err.value.decode()}")
+        return kind.value
+
     def set_roms(self, tsv: Optional[ReducedOrderModel] = None, dummy: Optional[ReducedOrderModel] = None):
         if tsv is not None:
             self.set_rom(0, tsv)

@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-O3",
     "--expt-relaxed-constexpr",
 ]
-SOURCES = ["context.cu", "local_stage.cu", "host_index.cpp"]
+SOURCES = ["context.cu", "local_stage.cu", "host_index.cpp", "rom_io.cpp"]
 LIBS = ["-lcusolver", "-lcublas", "-lcrypto", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 
 
