@@ -38,7 +38,8 @@ typedef enum {
 typedef enum { /* linalg::Precond, linalg.hpp:117 */
     TSV_PRECOND_NONE = 0,
     TSV_PRECOND_DIAGONAL = 1,
-    TSV_PRECOND_BLOCK_DIAGONAL = 2
+    TSV_PRECOND_BLOCK_DIAGONAL = 2,
+    TSV_PRECOND_SCHWARZ2 = 3    /* new: two-level additive Schwarz (per-block local solves + super-block coarse space) */
 } tsv_precond;
 
 typedef enum { TSV_KIND_TSV = 0, TSV_KIND_DUMMY = 1 } tsv_block_kind; /* BlockKind, mesh.hpp:43 */
@@ -85,6 +86,7 @@ typedef struct { /* GlobalSolution (global.hpp:91-96) + device timings */
     int best_iterations;      /* on TSV_ENOCONV: iteration of the returned best iterate */
     double solve_ms;          /* device time of the solve, CUDA events on the context stream */
     double loop_ms;           /* of which the iteration loop (excludes the best-iterate replay) */
+    int restarts;             /* true-residual verifications that failed and restarted CG (linalg.cpp:321-330) */
     uint64_t kernel_launches; /* kernels launched by this call */
 } tsv_solve_info;
 
@@ -147,6 +149,11 @@ int tsv_apply(tsv_ctx *ctx, const double *x, double *y);
  * on the GPU. u_out (N doubles, host) may be NULL: the solution stays
  * resident for tsv_recover*. On TSV_ENOCONV u_out holds the best iterate. */
 int tsv_solve(tsv_ctx *ctx, const tsv_iter_options *opts, double *u_out, tsv_solve_info *info);
+
+/* z = M^-1 r for the two-level Schwarz preconditioner (test hook). */
+int tsv_precond_apply(tsv_ctx *ctx, int precond, const double *r, double *z);
+/* Test hook: coarse-level vectors of the last tsv_precond_apply and A_c^-1 (any may be NULL). */
+int tsv_debug_coarse(tsv_ctx *ctx, int *nc, double *rc, double *zc, double *ainv_c);
 
 /* Make u (N doubles, host) the resident solution (recovery from given data). */
 int tsv_set_solution(tsv_ctx *ctx, const double *u);

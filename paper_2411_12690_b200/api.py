@@ -21,7 +21,7 @@ import numpy as np
 from . import native
 from .native import (TSV_EBREAKDOWN, TSV_ENOCONV, TSV_OK, IterOptionsC, RomDesc, SolveInfo, Timing)
 
-PRECOND = {"none": 0, "diagonal": 1, "block_diagonal": 2}
+PRECOND = {"none": 0, "diagonal": 1, "block_diagonal": 2, "schwarz2": 3}
 BC = {"bottom_pin": 0, "bottom_pin_321": 1, "clamped": 2, "none": 3}
 POINTS = {"gauss": 8, "centroid": 1}
 
@@ -116,6 +116,7 @@ class GlobalSolution:
     solve_ms: float = 0.0
     kernel_launches: int = 0
     loop_ms: float = 0.0
+    restarts: int = 0
 
 
 @dataclass
@@ -257,13 +258,19 @@ class GpuGlobalStage:
         self._check(self._L.tsv_apply(self._h, _p(x), _p(y)), "apply")
         return y
 
+    def precond_apply(self, r, precond: str = "schwarz2"):
+        r = np.ascontiguousarray(r, np.float64)
+        z = np.empty_like(r)
+        self._check(self._L.tsv_precond_apply(self._h, PRECOND[precond], _p(r), _p(z)), "precond_apply")
+        return z
+
     def solve_global(self, opts: IterOptions = IterOptions(), copy_out: bool = True) -> GlobalSolution:
         o = IterOptionsC(float(opts.tolerance), int(opts.max_iterations), PRECOND[opts.precond])
         info = SolveInfo()
         u = np.empty(self.index().dof_count) if copy_out else None
         rc = self._L.tsv_solve(self._h, C.byref(o), _p(u), C.byref(info))
         sol = GlobalSolution(u, info.iterations, info.relative_residual, bool(info.direct_fallback),
-                             info.best_iterations, info.solve_ms, info.kernel_launches, info.loop_ms)
+                             info.best_iterations, info.solve_ms, info.kernel_launches, info.loop_ms, info.restarts)
         if rc == TSV_ENOCONV:
             raise NoConvergence(self._L.tsv_last_error(self._h).decode(), sol)
         self._check(rc, "solve_global")

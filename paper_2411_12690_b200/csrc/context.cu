@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -26,6 +27,12 @@
 #include "../../include/tsv_b200.h"
 #include "host_index.hpp"
 #include "kernels.cuh"
+#include "schwarz.cuh"
+
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <map>
+#include <unordered_map>
 
 using namespace tsvb200;
 
@@ -80,6 +87,13 @@ struct DevBuf {
 };
 
 size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+// Device -> host copy ordered after everything queued on `s` (the context
+// stream is non-blocking, so a plain cudaMemcpy would not wait for it).
+void d2h(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
 
 // Panel column of local reduced DoF a = 3 rank + c (rom.cpp:26-31 order):
 // component-major within a block row.
@@ -145,6 +159,16 @@ struct tsv_ctx {
     int k1s_grid = 0;
     bool k1_small = false;  // small arrays: 64 x 64 tiles keep every SM busy
     bool k1_streamk = false;  // large arrays: stream-K balanced K1
+    // two-level additive Schwarz (precond 3)
+    struct As2 {
+        int s = 0, SX = 0, SY = 0, Nc = 0, ncells = 0, ntypes = 0, step = 0;
+        size_t BL_pad = 0, mtiles = 0;
+        DevBuf<int> slots2, tile_type, cell_ptr, cell_node;
+        DevBuf<double> XL, ZL, z, cellpart, rc, zc, ainv_c, ainv_store;
+        DevBuf<const double *> ainv_tab;
+        DevBuf<short4> lat;
+        double setup_ms = 0.0;
+    } as2;
     bool sk_resident = false;
     DevBuf<int> sk_start, sk_flag;
     DevBuf<double> sk_work;
@@ -460,11 +484,333 @@ struct tsv_ctx {
                 for (int k = 0; k < 9; ++k) inv_int[k * nodes + in] = inv[k];
             }
             pre.upload(inv_int.data(), inv_int.size(), stream);
+        } else if (kind == TSV_PRECOND_SCHWARZ2) {
+            pre.alloc(1);
+            build_schwarz2();
         } else {
             pre.alloc(1);
         }
         pre_kind = kind;
         drop_graph();
+    }
+
+    // --------------------------------------------------- two-level Schwarz
+    struct SolverHandles {
+        cusolverDnHandle_t sol = nullptr;
+        cublasHandle_t blas = nullptr;
+        ~SolverHandles() {
+            if (sol) cusolverDnDestroy(sol);
+            if (blas) cublasDestroy(blas);
+        }
+    };
+
+    // Inverse of an SPD matrix (column-major n x n) on the device; result in dA_inv.
+    void spd_inverse(SolverHandles &h, const std::vector<double> &A, size_t nn, double *dA_inv) {
+        DevBuf<double> dA, dI;
+        DevBuf<int> info;
+        dA.upload(A.data(), nn * nn, stream);
+        std::vector<double> eye(nn * nn, 0.0);
+        for (size_t i = 0; i < nn; ++i) eye[i * nn + i] = 1.0;
+        CK(cudaMemcpyAsync(dA_inv, eye.data(), nn * nn * sizeof(double), cudaMemcpyHostToDevice, stream));
+        info.alloc(1);
+        int lwork = 0;
+        if (cusolverDnDpotrf_bufferSize(h.sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(nn), dA.ptr, static_cast<int>(nn),
+                                        &lwork) != CUSOLVER_STATUS_SUCCESS)
+            throw StatusError(TSV_ECUDA, "schwarz2: potrf buffer query failed");
+        DevBuf<double> work;
+        work.alloc(std::max(lwork, 1));
+        if (cusolverDnDpotrf(h.sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(nn), dA.ptr, static_cast<int>(nn), work.ptr,
+                             lwork, info.ptr) != CUSOLVER_STATUS_SUCCESS)
+            throw StatusError(TSV_ECUDA, "schwarz2: potrf failed");
+        int hinfo = 0;
+        CK(cudaMemcpyAsync(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        if (hinfo != 0) throw StatusError(TSV_EINVAL, "schwarz2: local/coarse matrix not positive definite");
+        if (cusolverDnDpotrs(h.sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(nn), static_cast<int>(nn), dA.ptr,
+                             static_cast<int>(nn), dA_inv, static_cast<int>(nn), info.ptr) != CUSOLVER_STATUS_SUCCESS)
+            throw StatusError(TSV_ECUDA, "schwarz2: potrs failed");
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    void build_schwarz2() {
+        const auto t0 = std::chrono::steady_clock::now();
+        SolverHandles h;
+        if (cusolverDnCreate(&h.sol) != CUSOLVER_STATUS_SUCCESS || cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS)
+            throw StatusError(TSV_ECUDA, "schwarz2: cuSOLVER/cuBLAS init failed");
+        cusolverDnSetStream(h.sol, stream);
+        cublasSetStream(h.blas, stream);
+        const uint32_t rows = layout.rows, cols = layout.cols;
+        const size_t nn = n / 3;
+        // --- 1. neighbourhood types (own kind, 8 neighbours' kinds / absent, constrained pattern)
+        std::map<std::vector<int>, int> sig_type;
+        std::vector<int> type_of(B), rep_of;
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t c = 0; c < cols; ++c) {
+                const size_t cell = static_cast<size_t>(r) * cols + c;
+                std::vector<int> sig;
+                sig.push_back(layout.kind_at(cell));
+                for (int dr = -1; dr <= 1; ++dr)
+                    for (int dc = -1; dc <= 1; ++dc) {
+                        if (!dr && !dc) continue;
+                        const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
+                        sig.push_back(rr < 0 || cc < 0 || rr >= rows || cc >= cols
+                                          ? -1
+                                          : layout.kind_at(static_cast<size_t>(rr) * cols + static_cast<size_t>(cc)));
+                    }
+                const uint32_t *dm = dofmap.data() + cell * n;
+                for (size_t a = 0; a < n; ++a)
+                    if (constrained[dm[a]]) sig.push_back(1000 + static_cast<int>(a));
+                auto it = sig_type.find(sig);
+                if (it == sig_type.end()) {
+                    it = sig_type.emplace(sig, static_cast<int>(rep_of.size())).first;
+                    rep_of.push_back(static_cast<int>(cell));
+                }
+                type_of[cell] = it->second;
+            }
+        const int T = static_cast<int>(rep_of.size());
+        as2.ntypes = T;
+        // --- 2. local matrices A_b = R_b A R_b^T (lifted) per type, inverted on the device
+        const size_t rowsK = round_up(n, kBN);
+        as2.ainv_store.alloc(static_cast<size_t>(T) * rowsK * ldk);
+        CK(cudaMemsetAsync(as2.ainv_store.ptr, 0, as2.ainv_store.count * sizeof(double), stream));
+        DevBuf<double> inv;
+        inv.alloc(n * n);
+        std::vector<double> A(n * n), hinv(n * n), packed(rowsK * ldk);
+        std::vector<const double *> tab(T);
+        for (int t = 0; t < T; ++t) {
+            const size_t cell = static_cast<size_t>(rep_of[t]);
+            const uint32_t r = static_cast<uint32_t>(cell / cols), c = static_cast<uint32_t>(cell % cols);
+            const uint32_t *dm = dofmap.data() + cell * n;
+            std::unordered_map<uint32_t, int> loc;
+            loc.reserve(2 * n);
+            for (size_t a = 0; a < n; ++a) loc[dm[a]] = static_cast<int>(a);
+            std::fill(A.begin(), A.end(), 0.0);
+            std::vector<int> idx(n);
+            for (int dr = -1; dr <= 1; ++dr)
+                for (int dc = -1; dc <= 1; ++dc) {
+                    const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
+                    if (rr < 0 || cc < 0 || rr >= rows || cc >= cols) continue;
+                    const size_t b2 = static_cast<size_t>(rr) * cols + static_cast<size_t>(cc);
+                    const uint32_t *dm2 = dofmap.data() + b2 * n;
+                    const std::vector<double> &K2 = rom[layout.kind_at(b2)].k_r;
+                    for (size_t a = 0; a < n; ++a) {
+                        auto f = loc.find(dm2[a]);
+                        idx[a] = f == loc.end() ? -1 : f->second;
+                    }
+                    for (size_t a = 0; a < n; ++a) {
+                        if (idx[a] < 0) continue;
+                        for (size_t q2 = 0; q2 < n; ++q2)
+                            if (idx[q2] >= 0) A[static_cast<size_t>(idx[q2]) * n + idx[a]] += K2[a * n + q2];  // col-major
+                    }
+                }
+            for (size_t a = 0; a < n; ++a)
+                if (constrained[dm[a]]) {
+                    for (size_t k = 0; k < n; ++k) A[a * n + k] = A[k * n + a] = 0.0;
+                    A[a * n + a] = 1.0;
+                }
+            spd_inverse(h, A, n, inv.ptr);
+            d2h(hinv.data(), inv.ptr, n * n * sizeof(double), stream);
+            std::fill(packed.begin(), packed.end(), 0.0);
+            for (size_t a = 0; a < n; ++a)
+                for (size_t k = 0; k < n; ++k) packed[pidx(a, nn) * ldk + pidx(k, nn)] = hinv[k * n + a];
+            double *dst = as2.ainv_store.ptr + static_cast<size_t>(t) * rowsK * ldk;
+            CK(cudaMemcpyAsync(dst, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+            tab[t] = dst;
+        }
+        as2.ainv_tab.upload(tab.data(), tab.size(), stream);
+        // --- 3. type-ordered panel rows (types padded to the small-GEMM tile height)
+        constexpr size_t BML = K1SmallCfg::BM;
+        std::vector<int> rowL(B, -1), tiles;
+        size_t row = 0;
+        for (int t = 0; t < T; ++t) {
+            const size_t first = row;
+            for (size_t cell = 0; cell < B; ++cell)
+                if (type_of[cell] == t) rowL[cell] = static_cast<int>(row++);
+            row = first + round_up(row - first, BML);
+            for (size_t k = first / BML; k < row / BML; ++k) tiles.push_back(t);
+        }
+        as2.BL_pad = row;
+        as2.mtiles = row / BML;
+        if (as2.BL_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
+        as2.tile_type.upload(tiles.data(), tiles.size(), stream);
+        std::vector<int> s2(nodes * 4, -1);
+        for (size_t cell = 0; cell < B; ++cell) {
+            const uint32_t *dm = dofmap.data() + cell * n;
+            for (size_t rank = 0; rank < nn; ++rank) {
+                int *sl = s2.data() + static_cast<size_t>(node_int_of_glob[dm[3 * rank] / 3]) * 4;
+                int k = 0;
+                while (sl[k] >= 0) ++k;
+                sl[k] = static_cast<int>(static_cast<size_t>(rowL[cell]) * ldk + rank);
+            }
+        }
+        as2.slots2.upload(s2.data(), s2.size(), stream);
+        as2.XL.alloc(as2.BL_pad * ldk);
+        as2.ZL.alloc(as2.BL_pad * ldk);
+        CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
+        as2.z.alloc(N);
+        // --- 4. coarse space: corners of s x s super-blocks, bottom/top planes
+        const uint32_t q = nl.n_x;
+        const size_t cap = getenv("TSV_AS_COARSE_MAX") ? std::strtoul(getenv("TSV_AS_COARSE_MAX"), nullptr, 10) : 8192;
+        int sb = getenv("TSV_AS_S") ? std::max(1, std::atoi(getenv("TSV_AS_S"))) : 1;
+        for (; !getenv("TSV_AS_S"); ++sb) {
+            const size_t SX = (cols + sb - 1) / sb, SY = (rows + sb - 1) / sb;
+            if ((SX + 1) * (SY + 1) * 6 <= cap || (SX == 1 && SY == 1)) break;
+        }
+        as2.s = sb;
+        as2.SX = static_cast<int>((cols + sb - 1) / sb);
+        as2.SY = static_cast<int>((rows + sb - 1) / sb);
+        as2.step = sb * static_cast<int>(q - 1);
+        as2.Nc = (as2.SX + 1) * (as2.SY + 1) * 6;
+        as2.ncells = as2.SX * as2.SY;
+        std::vector<short4> lat(nodes);
+        std::vector<std::vector<int>> cellnodes(static_cast<size_t>(as2.ncells));
+        for (size_t in = 0; in < nodes; ++in) {
+            const auto &L = index.lattice_of_node[node_glob_of_int[in]];
+            lat[in] = make_short4(static_cast<short>(L[0]), static_cast<short>(L[1]), static_cast<short>(L[2]), 0);
+            const int cx = std::min(static_cast<int>(L[0]) / as2.step, as2.SX - 1);
+            const int cy = std::min(static_cast<int>(L[1]) / as2.step, as2.SY - 1);
+            cellnodes[static_cast<size_t>(cy) * as2.SX + cx].push_back(static_cast<int>(in));
+        }
+        std::vector<int> cptr(1, 0), cnode;
+        for (auto &v : cellnodes) {
+            cnode.insert(cnode.end(), v.begin(), v.end());
+            cptr.push_back(static_cast<int>(cnode.size()));
+        }
+        as2.lat.upload(lat.data(), lat.size(), stream);
+        as2.cell_ptr.upload(cptr.data(), cptr.size(), stream);
+        as2.cell_node.upload(cnode.data(), cnode.size(), stream);
+        as2.cellpart.alloc(static_cast<size_t>(as2.ncells) * 24);
+        as2.rc.alloc(as2.Nc);
+        as2.zc.alloc(as2.Nc);
+        // Galerkin A_c = sum_b P_b^T K_b P_b, P_b relative to b's super cell,
+        // zero on constrained DoFs; identical P_b (same kind / offsets / mask)
+        // share one 24 x 24 product (cuBLAS).
+        const size_t Ncs = static_cast<size_t>(as2.Nc);
+        std::vector<double> Ac(Ncs * Ncs, 0.0);
+        std::map<std::vector<long>, std::vector<double>> prod;
+        std::vector<double> Pb(n * 24), KP(n * 24), Kc(24 * 24);
+        DevBuf<double> dK, dP, dKP, dKc;
+        dP.alloc(n * 24);
+        dKP.alloc(n * 24);
+        dKc.alloc(24 * 24);
+        int loaded_kind = -1;
+        const auto &snodes = nl.surface_nodes;
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t c = 0; c < cols; ++c) {
+                const size_t cell = static_cast<size_t>(r) * cols + c;
+                const uint32_t *dm = dofmap.data() + cell * n;
+                const int cx = static_cast<int>(c) / sb, cy = static_cast<int>(r) / sb;
+                const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step;
+                const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step, index.lat_y - 1);
+                const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (q - 1);
+                std::vector<long> key = {layout.kind_at(cell), bx - x0, x1 - x0, by - y0, y1 - y0};
+                for (size_t a = 0; a < n; ++a)
+                    if (constrained[dm[a]]) key.push_back(static_cast<long>(a));
+                auto it = prod.find(key);
+                if (it == prod.end()) {
+                    std::fill(Pb.begin(), Pb.end(), 0.0);
+                    for (size_t rank = 0; rank < nn; ++rank) {
+                        const double tx = static_cast<double>(bx + snodes[rank][0] - x0) / static_cast<double>(x1 - x0);
+                        const double ty = static_cast<double>(by + snodes[rank][1] - y0) / static_cast<double>(y1 - y0);
+                        const double tz = static_cast<double>(snodes[rank][2]) / static_cast<double>(q - 1);
+                        for (int k = 0; k < 8; ++k) {
+                            const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
+                            for (int comp = 0; comp < 3; ++comp) {
+                                const size_t a = 3 * rank + comp;
+                                if (!constrained[dm[a]]) Pb[(3 * k + comp) * n + a] = w;  // col-major n x 24
+                            }
+                        }
+                    }
+                    const int kd = layout.kind_at(cell);
+                    if (kd != loaded_kind) {
+                        dK.upload(rom[kd].k_r.data(), n * n, stream);  // row-major K = col-major K^T = K
+                        loaded_kind = kd;
+                    }
+                    dP.upload(Pb.data(), n * 24, stream);
+                    const double one = 1.0, zero = 0.0;
+                    const int ni = static_cast<int>(n);
+                    if (cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, ni, 24, ni, &one, dK.ptr, ni, dP.ptr, ni, &zero, dKP.ptr,
+                                    ni) != CUBLAS_STATUS_SUCCESS ||
+                        cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, 24, 24, ni, &one, dP.ptr, ni, dKP.ptr, ni, &zero,
+                                    dKc.ptr, 24) != CUBLAS_STATUS_SUCCESS)
+                        throw StatusError(TSV_ECUDA, "schwarz2: coarse Galerkin product failed");
+                    d2h(Kc.data(), dKc.ptr, 24 * 24 * sizeof(double), stream);
+                    it = prod.emplace(key, Kc).first;
+                }
+                const std::vector<double> &kc = it->second;
+                int cdof[24];
+                for (int k = 0; k < 8; ++k) {
+                    const int node = (((k >> 2) & 1) * (as2.SY + 1) + cy + ((k >> 1) & 1)) * (as2.SX + 1) + cx + (k & 1);
+                    for (int comp = 0; comp < 3; ++comp) cdof[3 * k + comp] = 3 * node + comp;
+                }
+                for (int i = 0; i < 24; ++i)
+                    for (int j = 0; j < 24; ++j) Ac[static_cast<size_t>(cdof[j]) * Ncs + cdof[i]] += kc[j * 24 + i];
+            }
+        for (size_t i = 0; i < Ncs; ++i) {
+            bool zero_row = true;
+            for (size_t j = 0; j < Ncs && zero_row; ++j) zero_row = Ac[j * Ncs + i] == 0.0;
+            if (zero_row) Ac[i * Ncs + i] = 1.0;  // coarse DoF with no free fine support
+        }
+        as2.ainv_c.alloc(Ncs * Ncs);
+        spd_inverse(h, Ac, Ncs, as2.ainv_c.ptr);  // symmetric: row-major == col-major
+        as2.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+
+    GemmParams local_gemm_params() {
+        GemmParams gp{};
+        gp.A = as2.XL.ptr;
+        gp.lda = static_cast<long long>(ldk);
+        gp.Bt_tab = as2.ainv_tab.ptr;
+        gp.tile_type = as2.tile_type.ptr;
+        gp.ldb = static_cast<long long>(ldk);
+        gp.C = as2.ZL.ptr;
+        gp.ldc = static_cast<long long>(ldk);
+        gp.m_tiles = static_cast<int>(as2.mtiles);
+        gp.n_tiles = static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
+        gp.k_chunks = static_cast<int>(ldk / K1SmallCfg::KC);
+        gp.n_valid = gp.n_store = static_cast<int>(n);
+        gp.done = &state.ptr->done;
+        gp.tile_counter = tile_counter.ptr;
+        return gp;
+    }
+
+    AsParams as_params() {
+        AsParams a{};
+        a.slots2 = as2.slots2.ptr;
+        a.XL = as2.XL.ptr;
+        a.ZL = as2.ZL.ptr;
+        a.z = as2.z.ptr;
+        a.lat = as2.lat.ptr;
+        a.step = as2.step;
+        a.SX = as2.SX;
+        a.SY = as2.SY;
+        a.lat_x = static_cast<int>(index.lat_x);
+        a.lat_y = static_cast<int>(index.lat_y);
+        a.qm1 = static_cast<int>(nl.n_z - 1);
+        a.cell_ptr = as2.cell_ptr.ptr;
+        a.cell_node = as2.cell_node.ptr;
+        a.ncells = as2.ncells;
+        a.cellpart = as2.cellpart.ptr;
+        a.rc = as2.rc.ptr;
+        a.zc = as2.zc.ptr;
+        a.ainv_c = as2.ainv_c.ptr;
+        a.Nc = as2.Nc;
+        return a;
+    }
+
+    // r update + two-level Schwarz z = M r (U', local GEMM, restriction,
+    // coarse solve, prolongation + r.z).
+    void launch_as_update_precond(const CgParams &q) {
+        AsParams a = as_params();
+        as_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        GemmParams gp = local_gemm_params();
+        gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+        as_restrict_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
+        as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, stream>>>(q, a);
+        as_coarse_gemv_kernel<<<(as2.Nc + 7) / 8, 256, 0, stream>>>(q, a);
+        as_z_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        launches += 6;
     }
 
     // ------------------------------------------------------------ kernels
@@ -536,16 +882,24 @@ struct tsv_ctx {
         q.precond = pre_kind;
         q.pre = pre.ptr;
         q.partial = partial.ptr;
+        q.zbuf = as2.z.ptr;
         return q;
     }
 
     void launch_iteration(const CgParams &q) {
         launch_k1(&state.ptr->done);
         cg_gather_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
-        cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        if (pre_kind == TSV_PRECOND_SCHWARZ2) {
+            launch_as_update_precond(q);
+        } else {
+            cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+            ++launches;
+        }
         cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
-        launches += 3;
+        launches += 2;
     }
+
+    int graph_kernels_per_iteration() const { return pre_kind == TSV_PRECOND_SCHWARZ2 ? 9 : 4; }
 
     void ensure_graph() {
         if (iter_graph) return;
@@ -565,7 +919,7 @@ struct tsv_ctx {
         if (!layout_set) throw StatusError(TSV_ESTATE, "solve: no layout set");
         if (!(o.tolerance > 0.0)) throw StatusError(TSV_EINVAL, "IterOptions: tolerance must be > 0");
         if (o.max_iterations < 1) throw StatusError(TSV_EINVAL, "IterOptions: max_iterations must be >= 1");
-        if (o.precond < 0 || o.precond > 2) throw StatusError(TSV_EINVAL, "IterOptions: unknown preconditioner");
+        if (o.precond < 0 || o.precond > 3) throw StatusError(TSV_EINVAL, "IterOptions: unknown preconditioner");
         build_precond(o.precond);
         const uint64_t l0 = launches;
         CK(cudaEventRecord(ev0, stream));
@@ -603,7 +957,7 @@ struct tsv_ctx {
         solution_valid = true;
         if (u_out) {
             std::vector<double> xi(N);
-            CK(cudaMemcpy(xi.data(), x.ptr, N * sizeof(double), cudaMemcpyDeviceToHost));
+            d2h(xi.data(), x.ptr, N * sizeof(double), stream);
             to_reference(xi.data(), u_out);
         }
         if (info) {
@@ -613,6 +967,7 @@ struct tsv_ctx {
             info->best_iterations = best_it;
             info->solve_ms = ms;
             info->loop_ms = loop_ms;
+            info->restarts = st.restarts;
             info->kernel_launches = launches - l0;
         }
         if (status == TSV_ENOCONV) {
@@ -636,13 +991,18 @@ struct tsv_ctx {
         CK(cudaMemcpyAsync(state.ptr, h_state, sizeof(CgState), cudaMemcpyHostToDevice, stream));
         CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), stream));
         CgParams q = cg_params();
-        cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        if (pre_kind == TSV_PRECOND_SCHWARZ2) {
+            launch_as_update_precond(q);
+        } else {
+            cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+            ++launches;
+        }
         cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
-        launches += 2;
+        ++launches;
         CK(cudaGetLastError());
         // Host-polled batches of graph-captured iterations; a finished
         // solve turns the remaining launches into early exits.
-        const int graph_nodes = 4 * kItersPerGraph;
+        const int graph_nodes = graph_kernels_per_iteration() * kItersPerGraph;
         for (;;) {
             CK(cudaGraphLaunch(iter_graph, stream));
             launches += graph_nodes;
@@ -1105,7 +1465,7 @@ int tsv_get_load(tsv_ctx *ctx, double *bout) {
         if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_load: no layout set");
         cudaSetDevice(ctx->device);
         std::vector<double> bi(ctx->N);
-        CK(cudaMemcpy(bi.data(), ctx->b.ptr, ctx->N * sizeof(double), cudaMemcpyDeviceToHost));
+        d2h(bi.data(), ctx->b.ptr, ctx->N * sizeof(double), ctx->stream);
         ctx->to_reference(bi.data(), bout);
         return TSV_OK;
     });
@@ -1128,6 +1488,46 @@ int tsv_apply(tsv_ctx *ctx, const double *xin, double *yout) {
         CK(cudaMemcpyAsync(yi.data(), ctx->ap.ptr, ctx->N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         ctx->to_reference(yi.data(), yout);
+        return TSV_OK;
+    });
+}
+
+int tsv_precond_apply(tsv_ctx *ctx, int precond, const double *r_in, double *z_out) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "precond_apply: no layout set");
+        if (precond != TSV_PRECOND_SCHWARZ2) throw StatusError(TSV_EINVAL, "precond_apply: only the Schwarz preconditioner");
+        cudaSetDevice(ctx->device);
+        ctx->build_precond(precond);
+        std::vector<double> ri = ctx->to_internal(r_in);
+        ctx->r.upload(ri.data(), ctx->N, ctx->stream);
+        CgState st{};
+        st.done = CG_RUNNING;
+        st.phase = PH_RESTART;  // use r as is
+        st.tol = 1.0;
+        st.max_it = 1;
+        *ctx->h_state = st;
+        CK(cudaMemcpyAsync(ctx->state.ptr, ctx->h_state, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
+        CgParams q = ctx->cg_params();
+        ctx->launch_as_update_precond(q);
+        CK(cudaGetLastError());
+        std::vector<double> zi(ctx->N);
+        CK(cudaMemcpyAsync(zi.data(), ctx->as2.z.ptr, ctx->N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->to_reference(zi.data(), z_out);
+        ctx->solution_valid = false;
+        return TSV_OK;
+    });
+}
+
+// Test hook: the coarse level of the last tsv_precond_apply (rc, zc) and A_c^-1.
+int tsv_debug_coarse(tsv_ctx *ctx, int *nc, double *rc, double *zc, double *ainv) {
+    return guarded(ctx, [&] {
+        if (!ctx->as2.rc.ptr) throw StatusError(TSV_ESTATE, "debug_coarse: no Schwarz preconditioner built");
+        const size_t Nc = static_cast<size_t>(ctx->as2.Nc);
+        if (nc) *nc = static_cast<int>(Nc);
+        if (rc) d2h(rc, ctx->as2.rc.ptr, Nc * sizeof(double), ctx->stream);
+        if (zc) d2h(zc, ctx->as2.zc.ptr, Nc * sizeof(double), ctx->stream);
+        if (ainv) d2h(ainv, ctx->as2.ainv_c.ptr, Nc * Nc * sizeof(double), ctx->stream);
         return TSV_OK;
     });
 }
@@ -1203,8 +1603,7 @@ int tsv_copy_stress(tsv_ctx *ctx, uint64_t c0, uint64_t c1, double *out) {
         if (c0 > c1 || c1 > ctx->B) throw StatusError(TSV_EINVAL, "copy_stress: cell range out of bounds");
         cudaSetDevice(ctx->device);
         const size_t per_cell = ctx->elems() * static_cast<size_t>(ctx->stress_points) * 7;
-        CK(cudaMemcpy(out, ctx->stress.ptr + c0 * per_cell, (c1 - c0) * per_cell * sizeof(double),
-                      cudaMemcpyDeviceToHost));
+        d2h(out, ctx->stress.ptr + c0 * per_cell, (c1 - c0) * per_cell * sizeof(double), ctx->stream);
         return TSV_OK;
     });
 }

@@ -27,6 +27,8 @@ struct GemmParams {
     const double *Bt[2];  // per block kind
     long long ldb;
     const uint8_t *tile_kind;  // per M tile
+    const double *const *Bt_tab;  // nullable: per-tile matrix table indexed by tile_type
+    const int *tile_type;         // per M tile (with Bt_tab)
     double *C;
     long long ldc;
     int m_tiles, n_tiles, k_chunks;
@@ -126,7 +128,8 @@ __device__ __forceinline__ void gemm_segment(const GemmParams &p, double *As, do
     const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
     const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
     const double *A0 = p.A + static_cast<long long>(mt) * Cfg::BM * p.lda;
-    const double *B0 = (kind ? p.Bt[1] : p.Bt[0]) + static_cast<long long>(nt) * Cfg::BN * p.ldb;
+    const double *Bbase = p.Bt_tab ? p.Bt_tab[p.tile_type[mt]] : (kind ? p.Bt[1] : p.Bt[0]);
+    const double *B0 = Bbase + static_cast<long long>(nt) * Cfg::BN * p.ldb;
 #pragma unroll
     for (int s = 0; s < Cfg::STAGES - 1; ++s) {
         if (kc0 + s < kc1)
@@ -320,7 +323,7 @@ struct CgState {
     int y_holds_x;  // 1: the next product is A x (true-residual verification)
     int phase;      // what the B kernel does this iteration
     int p_assign;   // 1: p = z (fresh start), 0: p = z + beta p
-    int it, best_it, max_it, breakdown_code;
+    int it, best_it, max_it, breakdown_code, restarts;
     double rho, alpha, beta, res, best_res, norm_b, tol, tol_abs;
     unsigned ticket_a, ticket_b;
 };
@@ -343,6 +346,7 @@ struct CgParams {
     int precond;        // 0 none, 1 diagonal, 2 3x3 node blocks
     const double *pre;  // inv_diag [3][node] or inverse node blocks [9][node]
     double *partial;    // [grid][2]
+    const double *zbuf; // precond 3 (two-level Schwarz): z = M r computed by as_z_kernel
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -474,6 +478,7 @@ __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
         } else {
             st->res = sqrt(tot[0]);
             if (st->res <= st->tol_abs) st->done = CG_CONVERGED;
+            else st->restarts += 1;
             st->phase = PH_RESTART;
         }
         __threadfence();
@@ -579,9 +584,14 @@ __global__ void __launch_bounds__(256) cg_scatter_kernel(CgParams q) {
     const int N = q.n_nodes;
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         double r3[3], z3[3];
+        if (q.precond == 3) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) r3[c] = q.r[static_cast<long long>(c) * N + node];
-        precond_node(q.precond, q.pre, node, N, r3, z3);
+            for (int c = 0; c < 3; ++c) z3[c] = q.zbuf[static_cast<long long>(c) * N + node];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) r3[c] = q.r[static_cast<long long>(c) * N + node];
+            precond_node(q.precond, q.pre, node, N, r3, z3);
+        }
         const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {

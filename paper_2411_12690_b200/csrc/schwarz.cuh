@@ -1,0 +1,265 @@
+// Two-level additive Schwarz preconditioner for the reduced system
+// (TSV_PRECOND_SCHWARZ2, new: the reference offers none / Jacobi / 3x3
+// blocks, linalg.hpp:117; a stronger preconditioner is allowed when the
+// solution parity holds).
+//
+//   z = sum_b R_b^T A_b^-1 R_b r  +  P A_c^-1 P^T r
+//
+//   local:  A_b = R_b A R_b^T, the lifted global matrix restricted to block
+//           b's interface DoFs. It depends only on the block's neighbourhood
+//           (own kind, the 8 neighbours' kinds or absence, constrained
+//           pattern), so blocks are grouped into types and the local solves
+//           are one batched DMMA GEMM over a type-ordered panel.
+//   coarse: trilinear interpolation P from the corner lattice of s x s
+//           super-blocks (x, y) and the bottom/top planes (z); A_c = P^T A P
+//           is assembled from per-block 24 x 24 Galerkin products and
+//           inverted once (dense, <= 8192 DoFs); the coarse solve is a dense
+//           GEMV. P is zero on constrained DoFs.
+//
+// All reductions are fixed-order (deterministic).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace tsvb200 {
+
+struct AsParams {
+    const int *slots2;     // [node][4] offsets into XL / ZL (type-ordered panel rows)
+    double *XL;            // local-solve operand panel
+    const double *ZL;      // local-solve product panel
+    double *z;             // [3][node] preconditioned residual
+    const short4 *lat;     // (gx, gy, gz) lattice position of each internal node
+    int step, SX, SY, lat_x, lat_y, qm1;
+    const int *cell_ptr;   // super cell -> range of cell_node
+    const int *cell_node;  // internal nodes grouped by super cell
+    int ncells;
+    double *cellpart;      // [ncells][24]
+    double *rc, *zc;       // coarse vectors [Nc]
+    const double *ainv_c;  // dense [Nc][Nc]
+    int Nc;
+};
+
+__device__ __forceinline__ void as_cell_weights(const AsParams &a, int node, int &cx, int &cy, double w[8]) {
+    const short4 L = a.lat[node];
+    cx = min(static_cast<int>(L.x) / a.step, a.SX - 1);
+    cy = min(static_cast<int>(L.y) / a.step, a.SY - 1);
+    const int x0 = cx * a.step, x1 = min(x0 + a.step, a.lat_x - 1);
+    const int y0 = cy * a.step, y1 = min(y0 + a.step, a.lat_y - 1);
+    const double tx = static_cast<double>(L.x - x0) / static_cast<double>(x1 - x0);
+    const double ty = static_cast<double>(L.y - y0) / static_cast<double>(y1 - y0);
+    const double tz = static_cast<double>(L.z) / static_cast<double>(a.qm1);
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        w[c] = ((c & 1) ? tx : 1.0 - tx) * ((c & 2) ? ty : 1.0 - ty) * ((c & 4) ? tz : 1.0 - tz);
+}
+
+__device__ __forceinline__ int as_corner_node(const AsParams &a, int cx, int cy, int c) {
+    return (((c >> 2) & 1) * (a.SY + 1) + cy + ((c >> 1) & 1)) * (a.SX + 1) + cx + (c & 1);
+}
+
+// U': x += alpha p, r -= alpha Ap (NORMAL) | r = b (INIT) | r as is (RESTART);
+// r scattered into the local-solve panel; r.r reduced; the last CTA runs
+// the loop-head bookkeeping of cg_solve (iteration count, best iterate,
+// max-iteration exit, next product = A x when the residual test passes).
+__global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) {
+    __shared__ double sh[64];
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int phase = st->phase;
+    const double alpha = st->alpha;
+    const int N = q.n_nodes;
+    double part[1] = {0.0};
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+        const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            double rv;
+            if (phase == PH_NORMAL) {
+                q.x[dof] += alpha * q.p[dof];
+                rv = q.r[dof] - alpha * q.ap[dof];
+                q.r[dof] = rv;
+            } else if (phase == PH_INIT) {
+                q.x[dof] = 0.0;
+                rv = q.b[dof];
+                q.r[dof] = rv;
+            } else {
+                rv = q.r[dof];
+            }
+            part[0] += rv * rv;
+            if (q.cmask[dof]) continue;
+            const int co = c * q.nn;
+            if (s.x >= 0) a.XL[s.x + co] = rv;
+            if (s.y >= 0) a.XL[s.y + co] = rv;
+            if (s.z >= 0) a.XL[s.z + co] = rv;
+            if (s.w >= 0) a.XL[s.w + co] = rv;
+        }
+    }
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial, &st->ticket_b)) return;
+    double tot[1];
+    grid_sum<1>(q.partial, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_b = 0u;
+    if (phase == PH_INIT) {
+        st->norm_b = sqrt(tot[0]);
+        st->tol_abs = st->tol * st->norm_b;
+        st->res = st->norm_b;
+        st->best_res = st->res;
+        st->best_it = 0;
+        st->it = 0;
+        if (!isfinite(st->norm_b)) {
+            st->done = CG_BREAKDOWN;
+            st->breakdown_code = 1;
+        } else if (st->norm_b == 0.0) {
+            st->done = CG_CONVERGED;
+        } else {
+            st->y_holds_x = st->res <= st->tol_abs ? 1 : 0;
+        }
+    } else if (phase == PH_RESTART) {
+        st->y_holds_x = 0;
+    } else {
+        st->res = sqrt(tot[0]);
+        if (!isfinite(st->res)) {
+            st->done = CG_BREAKDOWN;
+            st->breakdown_code = 1;
+        } else {
+            st->it += 1;
+            if (st->res < st->best_res) {
+                st->best_res = st->res;
+                st->best_it = st->it;
+            }
+            if (st->it >= st->max_it) {
+                st->done = (st->res / st->norm_b <= st->tol) ? CG_CONVERGED : CG_NOCONV;
+            } else {
+                st->y_holds_x = st->res <= st->tol_abs ? 1 : 0;
+            }
+        }
+    }
+    __threadfence();
+}
+
+// Restriction, per super cell: partial P^T r over the cell's nodes (24 values).
+__global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a) {
+    __shared__ double sh[8][24];
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    const int cell = blockIdx.x;
+    const int N = q.n_nodes;
+    double acc[24];
+#pragma unroll
+    for (int k = 0; k < 24; ++k) acc[k] = 0.0;
+    for (int i = a.cell_ptr[cell] + threadIdx.x; i < a.cell_ptr[cell + 1]; i += blockDim.x) {
+        const int node = a.cell_node[i];
+        int cx, cy;
+        double w[8];
+        as_cell_weights(a, node, cx, cy, w);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            if (q.cmask[dof]) continue;
+            const double rv = q.r[dof];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[3 * k + c] += w[k] * rv;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 24; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (lane == 0) sh[warp][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 24) {
+        double s = 0.0;
+        for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) s += sh[w2][threadIdx.x];
+        a.cellpart[cell * 24 + threadIdx.x] = s;
+    }
+}
+
+// Coarse right-hand side: each coarse DoF sums its (up to 4) cells in order.
+__global__ void as_coarse_rhs_kernel(CgParams q, AsParams a) {
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= a.Nc) return;
+    const int comp = j % 3, cn = j / 3;
+    const int nxn = a.SX + 1, nyn = a.SY + 1;
+    const int gx = cn % nxn, gy = (cn / nxn) % nyn, gz = cn / (nxn * nyn);
+    double s = 0.0;
+    for (int cy = gy - 1; cy <= gy; ++cy) {
+        if (cy < 0 || cy >= a.SY) continue;
+        for (int cx = gx - 1; cx <= gx; ++cx) {
+            if (cx < 0 || cx >= a.SX) continue;
+            const int corner = (gx - cx) | ((gy - cy) << 1) | (gz << 2);
+            s += a.cellpart[(cy * a.SX + cx) * 24 + 3 * corner + comp];
+        }
+    }
+    a.rc[j] = s;
+}
+
+// Coarse solve: zc = A_c^-1 rc, one warp per row (fixed-order reduction).
+__global__ void as_coarse_gemv_kernel(CgParams q, AsParams a) {
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= a.Nc) return;
+    const double *m = a.ainv_c + static_cast<long long>(row) * a.Nc;
+    double s = 0.0;
+    for (int j = lane; j < a.Nc; j += 32) s += m[j] * a.rc[j];
+    s = warp_sum(s);
+    if (lane == 0) a.zc[row] = s;
+}
+
+// Z: z = sum of local products (owner gather) + P zc; (r.z) reduced; the
+// last CTA sets beta / rho (p = z + beta p, or p = z after init/restart).
+__global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
+    __shared__ double sh[64];
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int N = q.n_nodes;
+    double part[1] = {0.0};
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+        const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+        int cx, cy;
+        double w[8];
+        as_cell_weights(a, node, cx, cy, w);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            const double rv = q.r[dof];
+            double zv;
+            if (q.cmask[dof]) {
+                zv = rv;  // unit row of the lifted matrix
+            } else {
+                const int co = c * q.nn;
+                zv = 0.0;
+                if (s.x >= 0) zv += a.ZL[s.x + co];
+                if (s.y >= 0) zv += a.ZL[s.y + co];
+                if (s.z >= 0) zv += a.ZL[s.z + co];
+                if (s.w >= 0) zv += a.ZL[s.w + co];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) zv += w[k] * a.zc[3 * as_corner_node(a, cx, cy, k) + c];
+            }
+            a.z[dof] = zv;
+            part[0] += rv * zv;
+        }
+    }
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
+    double tot[1];
+    grid_sum<1>(q.partial, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_a = 0u;
+    const double rz = tot[0];
+    if (st->phase == PH_NORMAL) {
+        st->beta = rz / st->rho;
+        st->rho = rz;
+        st->p_assign = 0;
+    } else {  // INIT or RESTART: p = z
+        st->rho = rz;
+        st->p_assign = 1;
+        st->phase = PH_NORMAL;
+    }
+    __threadfence();
+}
+
+}  // namespace tsvb200
