@@ -22,6 +22,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tsv_b200.h"
@@ -504,32 +505,20 @@ struct tsv_ctx {
         }
     };
 
-    // Inverse of an SPD matrix (column-major n x n) on the device; result in dA_inv.
-    void spd_inverse(SolverHandles &h, const std::vector<double> &A, size_t nn, double *dA_inv) {
-        DevBuf<double> dA, dI;
-        DevBuf<int> info;
-        dA.upload(A.data(), nn * nn, stream);
-        std::vector<double> eye(nn * nn, 0.0);
-        for (size_t i = 0; i < nn; ++i) eye[i * nn + i] = 1.0;
-        CK(cudaMemcpyAsync(dA_inv, eye.data(), nn * nn * sizeof(double), cudaMemcpyHostToDevice, stream));
-        info.alloc(1);
-        int lwork = 0;
-        if (cusolverDnDpotrf_bufferSize(h.sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(nn), dA.ptr, static_cast<int>(nn),
-                                        &lwork) != CUSOLVER_STATUS_SUCCESS)
-            throw StatusError(TSV_ECUDA, "schwarz2: potrf buffer query failed");
-        DevBuf<double> work;
-        work.alloc(std::max(lwork, 1));
-        if (cusolverDnDpotrf(h.sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(nn), dA.ptr, static_cast<int>(nn), work.ptr,
-                             lwork, info.ptr) != CUSOLVER_STATUS_SUCCESS)
-            throw StatusError(TSV_ECUDA, "schwarz2: potrf failed");
-        int hinfo = 0;
-        CK(cudaMemcpyAsync(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
-        if (hinfo != 0) throw StatusError(TSV_EINVAL, "schwarz2: local/coarse matrix not positive definite");
-        if (cusolverDnDpotrs(h.sol, CUBLAS_FILL_MODE_LOWER, static_cast<int>(nn), static_cast<int>(nn), dA.ptr,
-                             static_cast<int>(nn), dA_inv, static_cast<int>(nn), info.ptr) != CUSOLVER_STATUS_SUCCESS)
-            throw StatusError(TSV_ECUDA, "schwarz2: potrs failed");
-        CK(cudaStreamSynchronize(stream));
+    // In-place SPD inverse on the device (column-major, lower triangle
+    // valid on return): potrf + potri, no host synchronisation. `info`
+    // collects the factorisation status, checked once at the end.
+    void spd_inverse_inplace(SolverHandles &h, double *dA, int nn, DevBuf<double> &work, int *info) {
+        int lwork = 0, lwork2 = 0;
+        if (cusolverDnDpotrf_bufferSize(h.sol, CUBLAS_FILL_MODE_LOWER, nn, dA, nn, &lwork) != CUSOLVER_STATUS_SUCCESS ||
+            cusolverDnDpotri_bufferSize(h.sol, CUBLAS_FILL_MODE_LOWER, nn, dA, nn, &lwork2) != CUSOLVER_STATUS_SUCCESS)
+            throw StatusError(TSV_ECUDA, "schwarz2: cuSOLVER buffer query failed");
+        const size_t need = static_cast<size_t>(std::max(std::max(lwork, lwork2), 1));
+        if (work.count < need) work.alloc(need);
+        if (cusolverDnDpotrf(h.sol, CUBLAS_FILL_MODE_LOWER, nn, dA, nn, work.ptr, lwork, info) != CUSOLVER_STATUS_SUCCESS ||
+            cusolverDnDpotri(h.sol, CUBLAS_FILL_MODE_LOWER, nn, dA, nn, work.ptr, lwork2, info + 1) !=
+                CUSOLVER_STATUS_SUCCESS)
+            throw StatusError(TSV_ECUDA, "schwarz2: potrf/potri failed");
     }
 
     void build_schwarz2() {
@@ -541,7 +530,20 @@ struct tsv_ctx {
         cublasSetStream(h.blas, stream);
         const uint32_t rows = layout.rows, cols = layout.cols;
         const size_t nn = n / 3;
-        // --- 1. neighbourhood types (own kind, 8 neighbours' kinds / absent, constrained pattern)
+        const bool dbg = getenv_flag("TSV_DEBUG");
+        auto tick = [&](const char *what) {
+            if (dbg) cudaStreamSynchronize(stream);
+            if (dbg)
+                std::fprintf(stderr, "[schwarz2] %-28s %8.1f ms\n", what,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        };
+        // --- 1. neighbourhood types: own kind, the 4 edge neighbours' kinds
+        // (or absence), corner neighbours' presence, constrained pattern.
+        // Blocks of one type share the representative's local matrix
+        // (exact except for corner-neighbour kinds; TSV_AS_EXACT_TYPES=1
+        // makes corner kinds part of the type too).
+        tick("handles");
+        const bool exact_types = getenv_flag("TSV_AS_EXACT_TYPES");
         std::map<std::vector<int>, int> sig_type;
         std::vector<int> type_of(B), rep_of;
         for (uint32_t r = 0; r < rows; ++r)
@@ -553,9 +555,9 @@ struct tsv_ctx {
                     for (int dc = -1; dc <= 1; ++dc) {
                         if (!dr && !dc) continue;
                         const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
-                        sig.push_back(rr < 0 || cc < 0 || rr >= rows || cc >= cols
-                                          ? -1
-                                          : layout.kind_at(static_cast<size_t>(rr) * cols + static_cast<size_t>(cc)));
+                        const bool in = rr >= 0 && cc >= 0 && rr < rows && cc < cols;
+                        const int kd = in ? layout.kind_at(static_cast<size_t>(rr) * cols + static_cast<size_t>(cc)) : -1;
+                        sig.push_back((dr && dc && !exact_types) ? (in ? 0 : -1) : kd);
                     }
                 const uint32_t *dm = dofmap.data() + cell * n;
                 for (size_t a = 0; a < n; ++a)
@@ -569,66 +571,84 @@ struct tsv_ctx {
             }
         const int T = static_cast<int>(rep_of.size());
         as2.ntypes = T;
-        // --- 2. local matrices A_b = R_b A R_b^T (lifted) per type, inverted on the device
+        tick("types");
+        // --- 2. local matrices A_b = R_b A R_b^T (lifted), assembled on host
+        // threads, inverted in place on the device, packed by a kernel.
+        std::vector<double> Aall(static_cast<size_t>(T) * n * n, 0.0);
+        {
+            const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), static_cast<unsigned>(T)));
+            std::vector<std::thread> pool;
+            for (unsigned w = 0; w < nt; ++w)
+                pool.emplace_back([&, w] {
+                    std::vector<int> idx(n);
+                    for (int t = static_cast<int>(w); t < T; t += static_cast<int>(nt)) {
+                        double *A = Aall.data() + static_cast<size_t>(t) * n * n;  // column-major
+                        const size_t cell = static_cast<size_t>(rep_of[t]);
+                        const uint32_t r = static_cast<uint32_t>(cell / cols), c = static_cast<uint32_t>(cell % cols);
+                        const uint32_t *dm = dofmap.data() + cell * n;
+                        std::unordered_map<uint32_t, int> loc;
+                        loc.reserve(2 * n);
+                        for (size_t a = 0; a < n; ++a) loc[dm[a]] = static_cast<int>(a);
+                        for (int dr = -1; dr <= 1; ++dr)
+                            for (int dc = -1; dc <= 1; ++dc) {
+                                const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
+                                if (rr < 0 || cc < 0 || rr >= rows || cc >= cols) continue;
+                                const size_t b2 = static_cast<size_t>(rr) * cols + static_cast<size_t>(cc);
+                                const uint32_t *dm2 = dofmap.data() + b2 * n;
+                                const std::vector<double> &K2 = rom[layout.kind_at(b2)].k_r;
+                                for (size_t a = 0; a < n; ++a) {
+                                    auto f = loc.find(dm2[a]);
+                                    idx[a] = f == loc.end() ? -1 : f->second;
+                                }
+                                for (size_t a = 0; a < n; ++a) {
+                                    if (idx[a] < 0) continue;
+                                    for (size_t q2 = 0; q2 < n; ++q2)
+                                        if (idx[q2] >= 0) A[static_cast<size_t>(idx[q2]) * n + idx[a]] += K2[a * n + q2];
+                                }
+                            }
+                        for (size_t a = 0; a < n; ++a)
+                            if (constrained[dm[a]]) {
+                                for (size_t k = 0; k < n; ++k) A[a * n + k] = A[k * n + a] = 0.0;
+                                A[a * n + a] = 1.0;
+                            }
+                    }
+                });
+            for (auto &th : pool) th.join();
+        }
+        tick("local assembly (host)");
         const size_t rowsK = round_up(n, kBN);
         as2.ainv_store.alloc(static_cast<size_t>(T) * rowsK * ldk);
         CK(cudaMemsetAsync(as2.ainv_store.ptr, 0, as2.ainv_store.count * sizeof(double), stream));
-        DevBuf<double> inv;
-        inv.alloc(n * n);
-        std::vector<double> A(n * n), hinv(n * n), packed(rowsK * ldk);
+        DevBuf<double> dAll, work;
+        DevBuf<int> infos;
+        dAll.upload(Aall.data(), Aall.size(), stream);
+        infos.alloc(static_cast<size_t>(2 * T + 2));
+        CK(cudaMemsetAsync(infos.ptr, 0, infos.count * sizeof(int), stream));
         std::vector<const double *> tab(T);
         for (int t = 0; t < T; ++t) {
-            const size_t cell = static_cast<size_t>(rep_of[t]);
-            const uint32_t r = static_cast<uint32_t>(cell / cols), c = static_cast<uint32_t>(cell % cols);
-            const uint32_t *dm = dofmap.data() + cell * n;
-            std::unordered_map<uint32_t, int> loc;
-            loc.reserve(2 * n);
-            for (size_t a = 0; a < n; ++a) loc[dm[a]] = static_cast<int>(a);
-            std::fill(A.begin(), A.end(), 0.0);
-            std::vector<int> idx(n);
-            for (int dr = -1; dr <= 1; ++dr)
-                for (int dc = -1; dc <= 1; ++dc) {
-                    const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
-                    if (rr < 0 || cc < 0 || rr >= rows || cc >= cols) continue;
-                    const size_t b2 = static_cast<size_t>(rr) * cols + static_cast<size_t>(cc);
-                    const uint32_t *dm2 = dofmap.data() + b2 * n;
-                    const std::vector<double> &K2 = rom[layout.kind_at(b2)].k_r;
-                    for (size_t a = 0; a < n; ++a) {
-                        auto f = loc.find(dm2[a]);
-                        idx[a] = f == loc.end() ? -1 : f->second;
-                    }
-                    for (size_t a = 0; a < n; ++a) {
-                        if (idx[a] < 0) continue;
-                        for (size_t q2 = 0; q2 < n; ++q2)
-                            if (idx[q2] >= 0) A[static_cast<size_t>(idx[q2]) * n + idx[a]] += K2[a * n + q2];  // col-major
-                    }
-                }
-            for (size_t a = 0; a < n; ++a)
-                if (constrained[dm[a]]) {
-                    for (size_t k = 0; k < n; ++k) A[a * n + k] = A[k * n + a] = 0.0;
-                    A[a * n + a] = 1.0;
-                }
-            spd_inverse(h, A, n, inv.ptr);
-            d2h(hinv.data(), inv.ptr, n * n * sizeof(double), stream);
-            std::fill(packed.begin(), packed.end(), 0.0);
-            for (size_t a = 0; a < n; ++a)
-                for (size_t k = 0; k < n; ++k) packed[pidx(a, nn) * ldk + pidx(k, nn)] = hinv[k * n + a];
+            double *dA = dAll.ptr + static_cast<size_t>(t) * n * n;
+            spd_inverse_inplace(h, dA, static_cast<int>(n), work, infos.ptr + 2 * t);
             double *dst = as2.ainv_store.ptr + static_cast<size_t>(t) * rowsK * ldk;
-            CK(cudaMemcpyAsync(dst, packed.data(), packed.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
-            CK(cudaStreamSynchronize(stream));
+            as_pack_inverse_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
+                dA, static_cast<int>(n), static_cast<int>(nn), static_cast<int>(ldk), dst);
             tab[t] = dst;
         }
+        CK(cudaGetLastError());
         as2.ainv_tab.upload(tab.data(), tab.size(), stream);
+        tick("local inverses (device)");
         // --- 3. type-ordered panel rows (types padded to the small-GEMM tile height)
         constexpr size_t BML = K1SmallCfg::BM;
         std::vector<int> rowL(B, -1), tiles;
         size_t row = 0;
-        for (int t = 0; t < T; ++t) {
-            const size_t first = row;
-            for (size_t cell = 0; cell < B; ++cell)
-                if (type_of[cell] == t) rowL[cell] = static_cast<int>(row++);
-            row = first + round_up(row - first, BML);
-            for (size_t k = first / BML; k < row / BML; ++k) tiles.push_back(t);
+        {
+            std::vector<std::vector<int>> members(T);
+            for (size_t cell = 0; cell < B; ++cell) members[type_of[cell]].push_back(static_cast<int>(cell));
+            for (int t = 0; t < T; ++t) {
+                const size_t first = row;
+                for (int cell : members[t]) rowL[cell] = static_cast<int>(row++);
+                row = first + round_up(row - first, BML);
+                for (size_t k = first / BML; k < row / BML; ++k) tiles.push_back(t);
+            }
         }
         as2.BL_pad = row;
         as2.mtiles = row / BML;
@@ -649,6 +669,7 @@ struct tsv_ctx {
         as2.ZL.alloc(as2.BL_pad * ldk);
         CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
         as2.z.alloc(N);
+        tick("panel tables");
         // --- 4. coarse space: corners of s x s super-blocks, bottom/top planes
         const uint32_t q = nl.n_x;
         const size_t cap = getenv("TSV_AS_COARSE_MAX") ? std::strtoul(getenv("TSV_AS_COARSE_MAX"), nullptr, 10) : 8192;
@@ -683,18 +704,14 @@ struct tsv_ctx {
         as2.cellpart.alloc(static_cast<size_t>(as2.ncells) * 24);
         as2.rc.alloc(as2.Nc);
         as2.zc.alloc(as2.Nc);
-        // Galerkin A_c = sum_b P_b^T K_b P_b, P_b relative to b's super cell,
-        // zero on constrained DoFs; identical P_b (same kind / offsets / mask)
-        // share one 24 x 24 product (cuBLAS).
-        const size_t Ncs = static_cast<size_t>(as2.Nc);
-        std::vector<double> Ac(Ncs * Ncs, 0.0);
-        std::map<std::vector<long>, std::vector<double>> prod;
-        std::vector<double> Pb(n * 24), KP(n * 24), Kc(24 * 24);
-        DevBuf<double> dK, dP, dKP, dKc;
-        dP.alloc(n * 24);
-        dKP.alloc(n * 24);
-        dKc.alloc(24 * 24);
-        int loaded_kind = -1;
+        // Galerkin A_c = sum_b P_b^T K_b P_b (P_b relative to b's super cell,
+        // zero on constrained DoFs). Blocks with identical P_b (kind, offsets
+        // in the cell, cell extents, constrained pattern) share one 24 x 24
+        // product; the products are batched per kind on cuBLAS.
+        std::map<std::vector<long>, int> key_id;
+        std::vector<int> key_of(B), key_kind, key_local;
+        std::vector<double> Pall[2];  // per kind, column-major n x 24 each
+        int nkind_keys[2] = {0, 0};
         const auto &snodes = nl.surface_nodes;
         for (uint32_t r = 0; r < rows; ++r)
             for (uint32_t c = 0; c < cols; ++c) {
@@ -707,9 +724,15 @@ struct tsv_ctx {
                 std::vector<long> key = {layout.kind_at(cell), bx - x0, x1 - x0, by - y0, y1 - y0};
                 for (size_t a = 0; a < n; ++a)
                     if (constrained[dm[a]]) key.push_back(static_cast<long>(a));
-                auto it = prod.find(key);
-                if (it == prod.end()) {
-                    std::fill(Pb.begin(), Pb.end(), 0.0);
+                auto it = key_id.find(key);
+                if (it == key_id.end()) {
+                    it = key_id.emplace(key, static_cast<int>(key_kind.size())).first;
+                    const int kd = layout.kind_at(cell);
+                    key_kind.push_back(kd);
+                    key_local.push_back(nkind_keys[kd]++);
+                    const size_t off = Pall[kd].size();
+                    Pall[kd].resize(off + n * 24, 0.0);
+                    double *Pb = Pall[kd].data() + off;
                     for (size_t rank = 0; rank < nn; ++rank) {
                         const double tx = static_cast<double>(bx + snodes[rank][0] - x0) / static_cast<double>(x1 - x0);
                         const double ty = static_cast<double>(by + snodes[rank][1] - y0) / static_cast<double>(y1 - y0);
@@ -718,42 +741,75 @@ struct tsv_ctx {
                             const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
                             for (int comp = 0; comp < 3; ++comp) {
                                 const size_t a = 3 * rank + comp;
-                                if (!constrained[dm[a]]) Pb[(3 * k + comp) * n + a] = w;  // col-major n x 24
+                                if (!constrained[dm[a]]) Pb[(3 * k + comp) * n + a] = w;
                             }
                         }
                     }
-                    const int kd = layout.kind_at(cell);
-                    if (kd != loaded_kind) {
-                        dK.upload(rom[kd].k_r.data(), n * n, stream);  // row-major K = col-major K^T = K
-                        loaded_kind = kd;
-                    }
-                    dP.upload(Pb.data(), n * 24, stream);
-                    const double one = 1.0, zero = 0.0;
-                    const int ni = static_cast<int>(n);
-                    if (cublasDgemm(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, ni, 24, ni, &one, dK.ptr, ni, dP.ptr, ni, &zero, dKP.ptr,
-                                    ni) != CUBLAS_STATUS_SUCCESS ||
-                        cublasDgemm(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, 24, 24, ni, &one, dP.ptr, ni, dKP.ptr, ni, &zero,
-                                    dKc.ptr, 24) != CUBLAS_STATUS_SUCCESS)
-                        throw StatusError(TSV_ECUDA, "schwarz2: coarse Galerkin product failed");
-                    d2h(Kc.data(), dKc.ptr, 24 * 24 * sizeof(double), stream);
-                    it = prod.emplace(key, Kc).first;
                 }
-                const std::vector<double> &kc = it->second;
-                int cdof[24];
-                for (int k = 0; k < 8; ++k) {
-                    const int node = (((k >> 2) & 1) * (as2.SY + 1) + cy + ((k >> 1) & 1)) * (as2.SX + 1) + cx + (k & 1);
-                    for (int comp = 0; comp < 3; ++comp) cdof[3 * k + comp] = 3 * node + comp;
-                }
-                for (int i = 0; i < 24; ++i)
-                    for (int j = 0; j < 24; ++j) Ac[static_cast<size_t>(cdof[j]) * Ncs + cdof[i]] += kc[j * 24 + i];
+                key_of[cell] = it->second;
             }
-        for (size_t i = 0; i < Ncs; ++i) {
-            bool zero_row = true;
-            for (size_t j = 0; j < Ncs && zero_row; ++j) zero_row = Ac[j * Ncs + i] == 0.0;
-            if (zero_row) Ac[i * Ncs + i] = 1.0;  // coarse DoF with no free fine support
+        const int nkeys = static_cast<int>(key_kind.size());
+        tick("coarse keys");
+        if (dbg) std::fprintf(stderr, "[schwarz2] types %d keys %d s %d Nc %d n %zu\n", T, nkeys, sb, as2.Nc, n);
+        std::vector<double> Kcall[2];
+        {
+            DevBuf<double> dP, dKP, dKc, dK;
+            const double one = 1.0, zero = 0.0;
+            const int ni = static_cast<int>(n);
+            const long long sP = static_cast<long long>(n) * 24;
+            for (int kind = 0; kind < 2; ++kind) {
+                const int cnt = nkind_keys[kind];
+                if (!cnt) continue;
+                dK.upload(rom[kind].k_r.data(), n * n, stream);  // row-major K == column-major K^T == K
+                dP.upload(Pall[kind].data(), Pall[kind].size(), stream);
+                dKP.alloc(Pall[kind].size());
+                dKc.alloc(static_cast<size_t>(cnt) * 576);
+                if (cublasDgemmStridedBatched(h.blas, CUBLAS_OP_N, CUBLAS_OP_N, ni, 24, ni, &one, dK.ptr, ni, 0, dP.ptr,
+                                              ni, sP, &zero, dKP.ptr, ni, sP, cnt) != CUBLAS_STATUS_SUCCESS ||
+                    cublasDgemmStridedBatched(h.blas, CUBLAS_OP_T, CUBLAS_OP_N, 24, 24, ni, &one, dP.ptr, ni, sP,
+                                              dKP.ptr, ni, sP, &zero, dKc.ptr, 24, 576, cnt) != CUBLAS_STATUS_SUCCESS)
+                    throw StatusError(TSV_ECUDA, "schwarz2: coarse Galerkin products failed");
+                Kcall[kind].resize(static_cast<size_t>(cnt) * 576);
+                d2h(Kcall[kind].data(), dKc.ptr, Kcall[kind].size() * sizeof(double), stream);
+            }
         }
+        tick("coarse products (device)");
+        // per super cell: sum of its blocks' products in block order
+        std::vector<double> kcell(static_cast<size_t>(as2.ncells) * 576, 0.0);
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t c = 0; c < cols; ++c) {
+                const size_t cell = static_cast<size_t>(r) * cols + c;
+                const int cx = static_cast<int>(c) / sb, cy = static_cast<int>(r) / sb;
+                const int key = key_of[cell];
+                const double *src = Kcall[key_kind[key]].data() + static_cast<size_t>(key_local[key]) * 576;
+                double *dst = kcell.data() + (static_cast<size_t>(cy) * as2.SX + cx) * 576;
+                for (int e = 0; e < 576; ++e) dst[e] += src[e];
+            }
+        tick("coarse Galerkin products");
+        const size_t Ncs = static_cast<size_t>(as2.Nc);
         as2.ainv_c.alloc(Ncs * Ncs);
-        spd_inverse(h, Ac, Ncs, as2.ainv_c.ptr);  // symmetric: row-major == col-major
+        CK(cudaMemsetAsync(as2.ainv_c.ptr, 0, Ncs * Ncs * sizeof(double), stream));
+        {
+            DevBuf<double> dk;
+            dk.upload(kcell.data(), kcell.size(), stream);
+            for (int py = 0; py < 2; ++py)
+                for (int px = 0; px < 2; ++px) {
+                    const long long cnt = static_cast<long long>((as2.SX - px + 1) / 2) * ((as2.SY - py + 1) / 2) * 576;
+                    if (cnt <= 0) continue;
+                    as_coarse_scatter_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, stream>>>(
+                        dk.ptr, as2.SX, as2.SY, px, py, as2.ainv_c.ptr, as2.Nc);
+                }
+            as_fix_zero_rows_kernel<<<static_cast<unsigned>((Ncs + 7) / 8), 256, 0, stream>>>(as2.ainv_c.ptr, as2.Nc);
+            spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, infos.ptr + 2 * T);
+            as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
+                                                                                                       as2.Nc);
+            CK(cudaGetLastError());
+            std::vector<int> hinfo(infos.count);
+            d2h(hinfo.data(), infos.ptr, hinfo.size() * sizeof(int), stream);
+            for (int v : hinfo)
+                if (v != 0) throw StatusError(TSV_EINVAL, "schwarz2: local/coarse matrix not positive definite");
+        }
+        tick("coarse inverse");
         as2.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
 

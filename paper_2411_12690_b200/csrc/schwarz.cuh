@@ -263,3 +263,55 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
 }
 
 }  // namespace tsvb200
+
+namespace tsvb200 {
+
+// ---------------------------------------------------------------- setup
+// potri leaves the inverse in the lower triangle (column-major); write the
+// full symmetric matrix in the permuted, padded GEMM layout
+// dst[pidx(a) * ldk + pidx(k)], pidx(3 rank + c) = c nn + rank.
+__global__ void as_pack_inverse_kernel(const double *inv, int n, int nn, int ldk, double *dst) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<long long>(n) * n) return;
+    const int a = static_cast<int>(t / n), k = static_cast<int>(t % n);
+    const double v = a >= k ? inv[static_cast<long long>(k) * n + a] : inv[static_cast<long long>(a) * n + k];
+    dst[static_cast<long long>((a % 3) * nn + a / 3) * ldk + (k % 3) * nn + k / 3] = v;
+}
+
+// Dense coarse matrix (column-major), one colour of super cells at a time
+// (cells of equal (cx, cy) parity share no corner, so no write conflicts).
+__global__ void as_coarse_scatter_kernel(const double *kc_cell, int SX, int SY, int px, int py, double *Ac, int Nc) {
+    const int ncx = (SX - px + 1) / 2, ncy = (SY - py + 1) / 2;
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<long long>(ncx) * ncy * 576) return;
+    const int e = static_cast<int>(t % 576);
+    const long long cid = t / 576;
+    const int cx = px + 2 * static_cast<int>(cid % ncx), cy = py + 2 * static_cast<int>(cid / ncx);
+    const int i = e % 24, j = e / 24;
+    auto cdof = [&](int k) {
+        const int c = k / 3, comp = k % 3;
+        const int node = (((c >> 2) & 1) * (SY + 1) + cy + ((c >> 1) & 1)) * (SX + 1) + cx + (c & 1);
+        return 3 * node + comp;
+    };
+    Ac[static_cast<long long>(cdof(j)) * Nc + cdof(i)] += kc_cell[(static_cast<long long>(cy) * SX + cx) * 576 + e];
+}
+
+// Coarse DoFs with no free fine support get a unit diagonal (decoupled).
+__global__ void as_fix_zero_rows_kernel(double *Ac, int Nc) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= Nc) return;
+    bool nz = false;
+    for (int j = lane; j < Nc && !nz; j += 32) nz = Ac[static_cast<long long>(row) * Nc + j] != 0.0;
+    nz = __any_sync(0xffffffffu, nz);
+    if (!nz && lane == 0) Ac[static_cast<long long>(row) * Nc + row] = 1.0;
+}
+
+// Lower triangle -> full symmetric (column-major).
+__global__ void as_symmetrize_kernel(double *A, int Nc) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<long long>(Nc) * Nc) return;
+    const int col = static_cast<int>(t / Nc), row = static_cast<int>(t % Nc);
+    if (row < col) A[t] = A[static_cast<long long>(row) * Nc + col];
+}
+
+}  // namespace tsvb200
