@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=10, help="side of the CPU sample sub-array")
+    ap.add_argument("--precond", default="schwarz2", choices=["schwarz2", "diagonal", "block_diagonal", "none"],
+                    help="GPU preconditioner (the reference arm always runs its default Jacobi)")
+    ap.add_argument("--no-jacobi-leg", action="store_true",
+                    help="skip the one-step Jacobi-PCG comparison leg reported beside a schwarz2 headline")
     return ap.parse_args()
 
 
@@ -171,6 +175,13 @@ def cpu_sample(cfg, rom_tsv, rom_dum, iters, side, threads):
             "seconds_per_array": total}
 
 
+def jacobi_iterations(cfg):
+    """Jacobi-PCG iteration count of the config (what the reference's CG runs),
+    recorded by a GPU run in profiles/iterations.json."""
+    it = json.load(open(ITER_RECORD)).get(cfg.name) if os.path.exists(ITER_RECORD) else None
+    return it or DEFAULT_ITERS.get(cfg.name, 1)
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -182,8 +193,7 @@ def run_reference(args, cfg, rank, world):
     if rank != 0:
         return 0
     from oracle import refpy
-    iters = json.load(open(ITER_RECORD)).get(cfg.name) if os.path.exists(ITER_RECORD) else None
-    iters = iters or DEFAULT_ITERS.get(cfg.name, 1)
+    iters = jacobi_iterations(cfg)
     threads = host_threads()
     # the reference's own local stage (rom::build_rom) produces its input ROM
     rom_tsv = refpy.build_rom(cfg.d, cfg.h, cfg.t, cfg.p, cfg.m_xy, cfg.m_z, cfg.q, 0, cfg.liner_e, threads)
@@ -220,8 +230,10 @@ def run_ours(args, cfg, rank, local_rank, world):
 
     rom_tsv, rom_dum, t_rom = build_inputs(cfg, dev)
     g, layout = make_stage(cfg, rom_tsv, rom_dum, dev)
-    opts = IterOptions(TOL, 100000, "diagonal")
+    opts = IterOptions(TOL, 100000, args.precond)
     ix = g.index()
+    # preconditioner set-up: once per layout (inside e2e, outside the resident step)
+    pinfo = g.precond_setup(args.precond)
 
     def step():
         sol = g.solve_global(opts, copy_out=False)
@@ -252,13 +264,29 @@ def run_ours(args, cfg, rank, local_rank, world):
     k1_flops = 2.0 * cfg.n ** 2 * cfg.B
     dmma_peak = ctypes_peak(L, dev)
 
+    # the same step with the reference's own Jacobi-PCG (one timed step): the
+    # per-iteration kernel path the reference's preconditioner implies
+    jacobi = None
+    if args.precond != "diagonal" and not args.no_jacobi_leg and world == 1:
+        jopts = IterOptions(TOL, 100000, "diagonal")
+        g.solve_global(jopts, copy_out=False)
+        sj = g.solve_global(jopts, copy_out=False)
+        g.recover_resident(cfg.points)
+        tj = g.timing()
+        jacobi = {"iterations": sj.iterations, "ms_per_step": tj.solve_ms + tj.recover_ms,
+                  "value": cfg.B / ((tj.solve_ms + tj.recover_ms) * 1e-3),
+                  "ms_per_iteration": tj.solve_ms / max(1, sj.iterations)}
+        rec_j = sj.iterations
+    else:
+        rec_j = iters if args.precond == "diagonal" else None
+
     # end to end through the C ABI with host buffers
     e2e = run_e2e(args, cfg, g, layout, opts, L, world, max_over_ranks, barrier) if args.e2e_steps > 0 else None
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         try:
-            cpu = cpu_sample(cfg, rom_tsv, rom_dum, iters, args.cpu_sample, host_threads())
+            cpu = cpu_sample(cfg, rom_tsv, rom_dum, rec_j or jacobi_iterations(cfg), args.cpu_sample, host_threads())
             cpu.pop("seconds_per_array", None)
         except Exception as e:  # oracle not built: report, do not fail the bench
             cpu = {"value": None, "unit": "blocks/s", "cores": host_threads(), "kind": "reference",
@@ -267,13 +295,19 @@ def run_ours(args, cfg, rank, local_rank, world):
         os.makedirs(os.path.dirname(ITER_RECORD), exist_ok=True)
         rec = json.load(open(ITER_RECORD)) if os.path.exists(ITER_RECORD) else {}
         rec = {k: v for k, v in rec.items() if not k.startswith("_")} | {k: v for k, v in rec.items() if k.startswith("_")}
-        rec[cfg.name] = iters
+        if rec_j:
+            rec[cfg.name] = rec_j
+        rec[f"{cfg.name}/{args.precond}"] = iters
         json.dump(rec, open(ITER_RECORD, "w"), indent=1, sort_keys=True)
 
-    flops_step = iters * 2.0 * cfg.n ** 2 * cfg.B + 2.0 * cfg.n_fine * cfg.n * cfg.B
+    schwarz = args.precond == "schwarz2"
+    gemms = 2 if schwarz else 1  # K1 (+ the batched local solves A_b^-1 r_b)
+    nc = pinfo["coarse_dofs"]
+    flops_step = iters * gemms * 2.0 * cfg.n ** 2 * cfg.B + 2.0 * cfg.n_fine * cfg.n * cfg.B
     out_bytes = cfg.B * cfg.elements * cfg.points * 7 * 8
     hbm_peak = measured_hbm()
-    t_roof_ms = 1e3 * (iters * (2.0 * cfg.n ** 2 * cfg.B / (dmma_peak * 1e12) + 104.0 * ix.dof_count / (hbm_peak * 1e9))
+    vec_bytes = (136.0 if schwarz else 104.0) * ix.dof_count + 8.0 * nc * nc
+    t_roof_ms = 1e3 * (iters * (gemms * 2.0 * cfg.n ** 2 * cfg.B / (dmma_peak * 1e12) + vec_bytes / (hbm_peak * 1e9))
                        + max(2.0 * cfg.n_fine * cfg.n * cfg.B / (dmma_peak * 1e12), out_bytes / (hbm_peak * 1e9)))
     line = {
         "metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world, "steps": args.steps,
@@ -281,7 +315,8 @@ def run_ours(args, cfg, rank, local_rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "blocks": cfg.B, "array": f"{cfg.rows}x{cfg.cols}", "reduced_dofs_per_block": cfg.n,
                    "global_dofs": ix.dof_count, "fine_dofs_per_block": cfg.n_fine, "points_per_element": cfg.points,
-                   "iterations": iters, "tol": TOL, "precond": "diagonal", "bc": BC,
+                   "iterations": iters, "tol": TOL, "precond": args.precond, "bc": BC,
+                   "coarse_dofs": nc if schwarz else None,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2: {out_bytes / 1e9:.1f} GB stress output + {ix.dof_count * 8 * 6 / 1e6:.0f} MB vectors per step"},
         "roofline": {"bound": "tensor", "achieved": k1_flops / (k1_ms * 1e-3) / 1e12, "peak": dmma_peak,
@@ -289,12 +324,15 @@ def run_ours(args, cfg, rank, local_rank, world):
                      "kernel": "gemm_nt_f64 (K1 operator apply, 2n^2 B FLOP per launch)",
                      "peak_source": "measured live: register-only DMMA.8x8x4 loop (tsv_fp64_peak); MEASURED_PEAKS.json has no FP64 entry"},
         "end_to_end_roofline": {"t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_step,
-                                "model": "iters*(2n^2B/P64 + 104N/BW) + max(2 n_fine n B/P64, 56 B/point/BW)",
+                                "model": ("iters*(2*2n^2B/P64 + (136N + 8Nc^2)/BW) + max(2 n_fine n B/P64, 56 B/point/BW)"
+                                          if schwarz else "iters*(2n^2B/P64 + 104N/BW) + max(2 n_fine n B/P64, 56 B/point/BW)"),
                                 "hbm_gbs": hbm_peak},
         "gflops": flops_step / (ms_step * 1e-3) / 1e9,
         "phase_ms": {"solve": solve_ms, "recover": recover_ms, "k1_per_launch": k1_ms,
                      "per_iteration": solve_ms / max(1, iters)},
         "rom_build_s": t_rom,
+        "precond": pinfo,
+        "jacobi_leg": jacobi,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -152,6 +152,17 @@ int tsv_solve(tsv_ctx *ctx, const tsv_iter_options *opts, double *u_out, tsv_sol
 
 /* z = M^-1 r for the two-level Schwarz preconditioner (test hook). */
 int tsv_precond_apply(tsv_ctx *ctx, int precond, const double *r, double *z);
+typedef struct { /* preconditioner set-up of the current layout */
+    double setup_ms;   /* host wall time of the build (0 when it was already built) */
+    int ntypes;        /* Schwarz: block neighbourhood types (local inverses) */
+    int coarse_dofs;   /* Schwarz: coarse-space size Nc */
+    int super_block;   /* Schwarz: super-block side s (blocks) */
+    int local_rows;    /* Schwarz: type-padded rows of the local-solve panel */
+} tsv_precond_info;
+/* Build the preconditioner for the current layout now (tsv_solve builds it
+ * on first use) and describe it. No reference counterpart: the reference
+ * builds its Jacobi/block preconditioners inside cg_solve (linalg.cpp:221-290). */
+int tsv_precond_setup(tsv_ctx *ctx, int precond, tsv_precond_info *out);
 /* Test hook: coarse-level vectors of the last tsv_precond_apply and A_c^-1 (any may be NULL). */
 int tsv_debug_coarse(tsv_ctx *ctx, int *nc, double *rc, double *zc, double *ainv_c);
 

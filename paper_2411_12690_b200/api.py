@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import native
-from .native import (TSV_EBREAKDOWN, TSV_ENOCONV, TSV_OK, IterOptionsC, RomDesc, SolveInfo, Timing)
+from .native import (TSV_EBREAKDOWN, TSV_ENOCONV, TSV_OK, IterOptionsC, PrecondInfo, RomDesc, SolveInfo, Timing)
 
 PRECOND = {"none": 0, "diagonal": 1, "block_diagonal": 2, "schwarz2": 3}
 BC = {"bottom_pin": 0, "bottom_pin_321": 1, "clamped": 2, "none": 3}
@@ -263,6 +263,14 @@ class GpuGlobalStage:
         z = np.empty_like(r)
         self._check(self._L.tsv_precond_apply(self._h, PRECOND[precond], _p(r), _p(z)), "precond_apply")
         return z
+
+    def precond_setup(self, precond: str = "schwarz2") -> dict:
+        """Build the preconditioner for the current layout now; returns its
+        set-up time and (Schwarz) shape."""
+        info = PrecondInfo()
+        self._check(self._L.tsv_precond_setup(self._h, PRECOND[precond], C.byref(info)), "precond_setup")
+        return {"setup_ms": info.setup_ms, "ntypes": info.ntypes, "coarse_dofs": info.coarse_dofs,
+                "super_block": info.super_block, "local_rows": info.local_rows}
 
     def solve_global(self, opts: IterOptions = IterOptions(), copy_out: bool = True) -> GlobalSolution:
         o = IterOptionsC(float(opts.tolerance), int(opts.max_iterations), PRECOND[opts.precond])

@@ -1575,6 +1575,30 @@ int tsv_precond_apply(tsv_ctx *ctx, int precond, const double *r_in, double *z_o
     });
 }
 
+int tsv_precond_setup(tsv_ctx *ctx, int precond, tsv_precond_info *out) {
+    return guarded(ctx, [&] {
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "precond_setup: no layout set");
+        if (precond < TSV_PRECOND_NONE || precond > TSV_PRECOND_SCHWARZ2)
+            throw StatusError(TSV_EINVAL, "precond_setup: unknown preconditioner");
+        cudaSetDevice(ctx->device);
+        const auto t0 = std::chrono::steady_clock::now();
+        const bool had = ctx->pre_kind == precond;
+        ctx->build_precond(precond);
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (out) {
+            *out = tsv_precond_info{};
+            out->setup_ms = had ? 0.0 : std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (precond == TSV_PRECOND_SCHWARZ2) {
+                out->ntypes = ctx->as2.ntypes;
+                out->coarse_dofs = ctx->as2.Nc;
+                out->super_block = ctx->as2.s;
+                out->local_rows = static_cast<int>(ctx->as2.BL_pad);
+            }
+        }
+        return TSV_OK;
+    });
+}
+
 // Test hook: the coarse level of the last tsv_precond_apply (rc, zc) and A_c^-1.
 int tsv_debug_coarse(tsv_ctx *ctx, int *nc, double *rc, double *zc, double *ainv) {
     return guarded(ctx, [&] {

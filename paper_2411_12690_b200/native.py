@@ -17,7 +17,7 @@ TSV_OK, TSV_EINVAL, TSV_ENOCONV, TSV_EBREAKDOWN, TSV_ECUDA, TSV_ENOMEM, TSV_ESTA
 EXPORTS = [
     "tsv_ctx_create", "tsv_ctx_destroy", "tsv_last_error", "tsv_abi_version", "tsv_set_rom", "tsv_set_layout",
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
-    "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_precond_apply", "tsv_debug_coarse", "tsv_solve", "tsv_set_solution", "tsv_recover",
+    "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_precond_apply", "tsv_precond_setup", "tsv_debug_coarse", "tsv_solve", "tsv_set_solution", "tsv_recover",
     "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
     "tsv_rom_dims", "tsv_build_rom", "tsv_load_rom_file", "tsv_save_rom_file", "tsv_host_register", "tsv_host_unregister", "tsv_fp64_peak",
 ]
@@ -47,6 +47,11 @@ class SolveInfo(C.Structure):
     _fields_ = [("iterations", C.c_int), ("relative_residual", C.c_double), ("direct_fallback", C.c_int),
                 ("best_iterations", C.c_int), ("solve_ms", C.c_double), ("loop_ms", C.c_double), ("restarts", C.c_int),
                 ("kernel_launches", C.c_uint64)]
+
+
+class PrecondInfo(C.Structure):
+    _fields_ = [("setup_ms", C.c_double), ("ntypes", C.c_int), ("coarse_dofs", C.c_int),
+                ("super_block", C.c_int), ("local_rows", C.c_int)]
 
 
 class LocalDesc(C.Structure):
@@ -98,6 +103,7 @@ def load(path: str = LIB_PATH):
         "tsv_apply": (i, [vp, vp, vp]),
         "tsv_precond_apply": (i, [vp, i, vp, vp]),
         "tsv_debug_coarse": (i, [vp, P(i), vp, vp, vp]),
+        "tsv_precond_setup": (i, [vp, i, vp]),
         "tsv_solve": (i, [vp, P(IterOptionsC), vp, P(SolveInfo)]),
         "tsv_set_solution": (i, [vp, vp]),
         "tsv_recover": (i, [vp, i, u64, u64, vp]),
