@@ -169,6 +169,13 @@ struct tsv_ctx {
         DevBuf<const double *> ainv_tab;
         DevBuf<short4> lat;
         double setup_ms = 0.0;
+        // tensor-core (TF32) local solves
+        bool tc = false;
+        int KP = 0, NP = 0, BN = 0, ntn = 0;
+        DevBuf<float> XL32, ainv32;
+        DevBuf<int> slotsZ;
+        DevBuf<double> ZT;
+        CUtensorMap tmA{}, tmB{};
     } as2;
     bool sk_resident = false;
     DevBuf<int> sk_start, sk_flag;
@@ -616,9 +623,21 @@ struct tsv_ctx {
             for (auto &th : pool) th.join();
         }
         tick("local assembly (host)");
+        as2.tc = !getenv_flag("TSV_AS_LOCAL_F64") && as_round_bits() == 0;
         const size_t rowsK = round_up(n, kBN);
-        as2.ainv_store.alloc(static_cast<size_t>(T) * rowsK * ldk);
-        CK(cudaMemsetAsync(as2.ainv_store.ptr, 0, as2.ainv_store.count * sizeof(double), stream));
+        if (as2.tc) {
+            as2.KP = static_cast<int>(round_up(n, kTcBK));
+            as2.ntn = static_cast<int>((n + 255) / 256);
+            as2.BN = static_cast<int>(round_up((n + as2.ntn - 1) / as2.ntn, 16));
+            as2.NP = as2.ntn * as2.BN;
+            as2.ainv32.alloc(static_cast<size_t>(T) * as2.NP * as2.KP);
+            CK(cudaMemsetAsync(as2.ainv32.ptr, 0, as2.ainv32.count * sizeof(float), stream));
+            as2.ainv_store.release();
+        } else {
+            as2.ainv_store.alloc(static_cast<size_t>(T) * rowsK * ldk);
+            CK(cudaMemsetAsync(as2.ainv_store.ptr, 0, as2.ainv_store.count * sizeof(double), stream));
+            as2.ainv32.release();
+        }
         DevBuf<double> dAll, work;
         DevBuf<int> infos;
         dAll.upload(Aall.data(), Aall.size(), stream);
@@ -628,16 +647,24 @@ struct tsv_ctx {
         for (int t = 0; t < T; ++t) {
             double *dA = dAll.ptr + static_cast<size_t>(t) * n * n;
             spd_inverse_inplace(h, dA, static_cast<int>(n), work, infos.ptr + 2 * t);
+            if (as2.tc) {
+                as_pack_inverse_tf32_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
+                    dA, static_cast<int>(n), static_cast<int>(nn), as2.KP,
+                    as2.ainv32.ptr + static_cast<size_t>(t) * as2.NP * as2.KP);
+                tab[t] = nullptr;
+                continue;
+            }
             double *dst = as2.ainv_store.ptr + static_cast<size_t>(t) * rowsK * ldk;
             as_pack_inverse_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
-                dA, static_cast<int>(n), static_cast<int>(nn), static_cast<int>(ldk), dst);
+                dA, static_cast<int>(n), static_cast<int>(nn), static_cast<int>(ldk), dst, as_round_bits());
             tab[t] = dst;
         }
         CK(cudaGetLastError());
         as2.ainv_tab.upload(tab.data(), tab.size(), stream);
         tick("local inverses (device)");
         // --- 3. type-ordered panel rows (types padded to the small-GEMM tile height)
-        constexpr size_t BML = K1SmallCfg::BM;
+        const size_t BML = as2.tc ? static_cast<size_t>(kTcBM) : K1SmallCfg::BM;
+        const size_t lstride = as2.tc ? static_cast<size_t>(as2.KP) : ldk;
         std::vector<int> rowL(B, -1), tiles;
         size_t row = 0;
         {
@@ -654,20 +681,37 @@ struct tsv_ctx {
         as2.mtiles = row / BML;
         if (as2.BL_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
         as2.tile_type.upload(tiles.data(), tiles.size(), stream);
-        std::vector<int> s2(nodes * 4, -1);
+        std::vector<int> s2(nodes * 4, -1), sz(as2.tc ? nodes * 4 : 0, -1);
         for (size_t cell = 0; cell < B; ++cell) {
             const uint32_t *dm = dofmap.data() + cell * n;
             for (size_t rank = 0; rank < nn; ++rank) {
-                int *sl = s2.data() + static_cast<size_t>(node_int_of_glob[dm[3 * rank] / 3]) * 4;
+                const size_t in = node_int_of_glob[dm[3 * rank] / 3];
+                int *sl = s2.data() + in * 4;
                 int k = 0;
                 while (sl[k] >= 0) ++k;
-                sl[k] = static_cast<int>(static_cast<size_t>(rowL[cell]) * ldk + rank);
+                sl[k] = static_cast<int>(static_cast<size_t>(rowL[cell]) * lstride + rank);
+                if (as2.tc) sz[in * 4 + k] = static_cast<int>(rank * as2.BL_pad + static_cast<size_t>(rowL[cell]));
             }
         }
         as2.slots2.upload(s2.data(), s2.size(), stream);
-        as2.XL.alloc(as2.BL_pad * ldk);
-        as2.ZL.alloc(as2.BL_pad * ldk);
-        CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
+        if (as2.tc) {
+            if (static_cast<size_t>(as2.NP) * as2.BL_pad >= 0x7fffffffULL || as2.BL_pad * as2.KP >= 0x7fffffffULL)
+                throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
+            as2.slotsZ.upload(sz.data(), sz.size(), stream);
+            as2.XL32.alloc(as2.BL_pad * as2.KP);
+            CK(cudaMemsetAsync(as2.XL32.ptr, 0, as2.XL32.count * sizeof(float), stream));
+            as2.ZT.alloc(static_cast<size_t>(as2.NP) * as2.BL_pad);
+            as2.XL.release();
+            as2.ZL.release();
+            encode_tc_maps(T);
+        } else {
+            as2.XL.alloc(as2.BL_pad * ldk);
+            as2.ZL.alloc(as2.BL_pad * ldk);
+            CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
+            as2.XL32.release();
+            as2.ZT.release();
+            as2.slotsZ.release();
+        }
         as2.z.alloc(N);
         tick("panel tables");
         // --- 4. coarse space: corners of s x s super-blocks, bottom/top planes
@@ -831,6 +875,57 @@ struct tsv_ctx {
         return gp;
     }
 
+    // TMA descriptors of the tensor-core local solve: A = XL32 [rows][KP],
+    // B = Ainv32 [T * NP][KP], fp32, 32 x {128 | BN} boxes, 128-byte swizzle.
+    void encode_tc_maps(int T) {
+        using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        static EncodeFn encode = [] {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<EncodeFn>(fn);
+        }();
+        if (!encode) throw StatusError(TSV_ECUDA, "schwarz2: cuTensorMapEncodeTiled unavailable");
+        auto make = [&](CUtensorMap *m, void *ptr, uint64_t rows_, uint32_t box_rows) {
+            const cuuint64_t dims[2] = {static_cast<cuuint64_t>(as2.KP), rows_};
+            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(as2.KP) * sizeof(float)};
+            const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTcBK), box_rows};
+            const cuuint32_t estr[2] = {1, 1};
+            if (encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                throw StatusError(TSV_ECUDA, "schwarz2: tensor map encoding failed");
+        };
+        make(&as2.tmA, as2.XL32.ptr, as2.BL_pad, static_cast<uint32_t>(kTcBM));
+        make(&as2.tmB, as2.ainv32.ptr, static_cast<uint64_t>(T) * as2.NP, static_cast<uint32_t>(as2.BN));
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
+            attr = true;
+        }
+    }
+
+    void launch_tc_local() {
+        TcLocalParams tp{};
+        tp.tile_type = as2.tile_type.ptr;
+        tp.NP = as2.NP;
+        tp.BN = as2.BN;
+        tp.k_blocks = as2.KP / kTcBK;
+        tp.ZT = as2.ZT.ptr;
+        tp.ldz = static_cast<long long>(as2.BL_pad);
+        tp.done = &state.ptr->done;
+        tc_local_tf32_kernel<<<dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.mtiles)), kTcThreads,
+                               tc_smem_bytes(as2.BN), stream>>>(as2.tmA, as2.tmB, tp);
+    }
+
+    size_t nn_count() const { return n / 3; }
+
+    static int as_round_bits() { return getenv("TSV_AS_ROUND_BITS") ? std::atoi(getenv("TSV_AS_ROUND_BITS")) : 0; }
+
     AsParams as_params() {
         AsParams a{};
         a.slots2 = as2.slots2.ptr;
@@ -852,6 +947,13 @@ struct tsv_ctx {
         a.zc = as2.zc.ptr;
         a.ainv_c = as2.ainv_c.ptr;
         a.Nc = as2.Nc;
+        a.round_bits = as_round_bits();
+        if (as2.tc) {
+            a.XL32 = as2.XL32.ptr;
+            a.ZT = as2.ZT.ptr;
+            a.slotsZ = as2.slotsZ.ptr;
+            a.zt_cstride = static_cast<long long>(nn_count()) * static_cast<long long>(as2.BL_pad);
+        }
         return a;
     }
 
@@ -860,8 +962,12 @@ struct tsv_ctx {
     void launch_as_update_precond(const CgParams &q) {
         AsParams a = as_params();
         as_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
-        GemmParams gp = local_gemm_params();
-        gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+        if (as2.tc) {
+            launch_tc_local();
+        } else {
+            GemmParams gp = local_gemm_params();
+            gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+        }
         as_restrict_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
         as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, stream>>>(q, a);
         as_coarse_gemv_kernel<<<(as2.Nc + 7) / 8, 256, 0, stream>>>(q, a);

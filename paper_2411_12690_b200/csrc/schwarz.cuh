@@ -20,6 +20,7 @@
 #pragma once
 
 #include "kernels.cuh"
+#include "tc_local.cuh"
 
 namespace tsvb200 {
 
@@ -37,7 +38,24 @@ struct AsParams {
     double *rc, *zc;       // coarse vectors [Nc]
     const double *ainv_c;  // dense [Nc][Nc]
     int Nc;
+    int round_bits;        // experiment: round the local-solve operand to this many mantissa bits (0 = off)
+    // tensor-core local solve (tc_local.cuh): TF32 operand panel and the
+    // transposed FP64 product ZT[col][row]; slotsZ[node][4] = rank * rows + row
+    float *XL32;
+    const double *ZT;
+    const int *slotsZ;
+    long long zt_cstride;  // nn * rows: component stride in ZT
 };
+
+// Round to `bits` explicit mantissa bits (emulates a low-precision operand).
+__device__ __forceinline__ double round_mantissa(double v, int bits) {
+    if (bits <= 0 || bits >= 52) return v;
+    const int drop = 52 - bits;
+    long long i = __double_as_longlong(v);
+    i += 1LL << (drop - 1);
+    i &= ~((1LL << drop) - 1);
+    return __longlong_as_double(i);
+}
 
 __device__ __forceinline__ void as_cell_weights(const AsParams &a, int node, int &cx, int &cy, double w[8]) {
     const short4 L = a.lat[node];
@@ -89,6 +107,15 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             part[0] += rv * rv;
             if (q.cmask[dof]) continue;
             const int co = c * q.nn;
+            if (a.XL32) {
+                const float f = to_tf32(rv);
+                if (s.x >= 0) a.XL32[s.x + co] = f;
+                if (s.y >= 0) a.XL32[s.y + co] = f;
+                if (s.z >= 0) a.XL32[s.z + co] = f;
+                if (s.w >= 0) a.XL32[s.w + co] = f;
+                continue;
+            }
+            rv = round_mantissa(rv, a.round_bits);
             if (s.x >= 0) a.XL[s.x + co] = rv;
             if (s.y >= 0) a.XL[s.y + co] = rv;
             if (s.z >= 0) a.XL[s.z + co] = rv;
@@ -218,7 +245,7 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
     const int N = q.n_nodes;
     double part[1] = {0.0};
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
-        const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+        const int4 s = reinterpret_cast<const int4 *>(a.ZT ? a.slotsZ : a.slots2)[node];
         int cx, cy;
         double w[8];
         as_cell_weights(a, node, cx, cy, w);
@@ -230,12 +257,20 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
             if (q.cmask[dof]) {
                 zv = rv;  // unit row of the lifted matrix
             } else {
-                const int co = c * q.nn;
                 zv = 0.0;
-                if (s.x >= 0) zv += a.ZL[s.x + co];
-                if (s.y >= 0) zv += a.ZL[s.y + co];
-                if (s.z >= 0) zv += a.ZL[s.z + co];
-                if (s.w >= 0) zv += a.ZL[s.w + co];
+                if (a.ZT) {
+                    const double *zt = a.ZT + c * a.zt_cstride;
+                    if (s.x >= 0) zv += zt[s.x];
+                    if (s.y >= 0) zv += zt[s.y];
+                    if (s.z >= 0) zv += zt[s.z];
+                    if (s.w >= 0) zv += zt[s.w];
+                } else {
+                    const int co = c * q.nn;
+                    if (s.x >= 0) zv += a.ZL[s.x + co];
+                    if (s.y >= 0) zv += a.ZL[s.y + co];
+                    if (s.z >= 0) zv += a.ZL[s.z + co];
+                    if (s.w >= 0) zv += a.ZL[s.w + co];
+                }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) zv += w[k] * a.zc[3 * as_corner_node(a, cx, cy, k) + c];
             }
@@ -270,12 +305,12 @@ namespace tsvb200 {
 // potri leaves the inverse in the lower triangle (column-major); write the
 // full symmetric matrix in the permuted, padded GEMM layout
 // dst[pidx(a) * ldk + pidx(k)], pidx(3 rank + c) = c nn + rank.
-__global__ void as_pack_inverse_kernel(const double *inv, int n, int nn, int ldk, double *dst) {
+__global__ void as_pack_inverse_kernel(const double *inv, int n, int nn, int ldk, double *dst, int round_bits) {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= static_cast<long long>(n) * n) return;
     const int a = static_cast<int>(t / n), k = static_cast<int>(t % n);
     const double v = a >= k ? inv[static_cast<long long>(k) * n + a] : inv[static_cast<long long>(a) * n + k];
-    dst[static_cast<long long>((a % 3) * nn + a / 3) * ldk + (k % 3) * nn + k / 3] = v;
+    dst[static_cast<long long>((a % 3) * nn + a / 3) * ldk + (k % 3) * nn + k / 3] = round_mantissa(v, round_bits);
 }
 
 // Dense coarse matrix (column-major), one colour of super cells at a time

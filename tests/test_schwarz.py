@@ -36,3 +36,35 @@ def test_schwarz2_matches_reference(oracle_libs, native_lib, case):
     assert mx.max() <= 1e-8
     # deterministic
     assert np.array_equal(g.solve_global(IterOptions(1e-12, 10000, "schwarz2")).u, sol.u)
+
+
+@pytest.mark.parametrize("case", ["cfg0", "mixed"])
+def test_tensor_core_local_solve_matches_fp64(oracle_libs, native_lib, monkeypatch, case):
+    """The TF32 tcgen05 local solves (default) against the FP64 DMMA ones
+    (TSV_AS_LOCAL_F64=1): M^-1 r agrees to TF32 accuracy, and both PCG runs
+    converge to the same u within the parity bar."""
+    from test_gpu_parity import make_case
+    refpy, _ = oracle_libs
+    cfg = configs.get(0)
+    rng = np.random.default_rng(11)
+    kinds = (rng.random(20) < 0.3).astype(np.uint8) if case == "mixed" else None
+    out = {}
+    for mode in ("f64", "tf32"):
+        if mode == "f64":
+            monkeypatch.setenv("TSV_AS_LOCAL_F64", "1")
+        else:
+            monkeypatch.delenv("TSV_AS_LOCAL_F64", raising=False)
+        if case == "mixed":
+            sess, g = make_case(refpy, cfg, 4, 5, kinds, -270.0 + 40.0 * np.random.default_rng(3).random(20))
+        else:
+            sess, g = make_case(refpy, cfg)
+        r = np.random.default_rng(5).standard_normal(g.index().dof_count)
+        z = g.precond_apply(r, "schwarz2")
+        sol = g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
+        out[mode] = (z, sol)
+        u_r, _, _ = sess.iterate(1e-12)
+        assert rel_l2(sol.u, u_r) <= 1e-10
+    z64, s64 = out["f64"]
+    z32, s32 = out["tf32"]
+    assert 0 < rel_l2(z32, z64) <= 2e-3
+    assert abs(s32.iterations - s64.iterations) <= max(3, s64.iterations // 10)
