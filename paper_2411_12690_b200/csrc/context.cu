@@ -176,6 +176,8 @@ struct tsv_ctx {
         DevBuf<int> slotsZ;
         DevBuf<double> ZT;
         CUtensorMap tmA{}, tmB{};
+        DevBuf<float> ainv_c32;
+        int ldc32 = 0;
     } as2;
     bool sk_resident = false;
     DevBuf<int> sk_start, sk_flag;
@@ -847,6 +849,15 @@ struct tsv_ctx {
             spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, infos.ptr + 2 * T);
             as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
                                                                                                        as2.Nc);
+            if (!getenv_flag("TSV_AS_COARSE_F64")) {
+                as2.ldc32 = static_cast<int>(round_up(Ncs, 32));
+                as2.ainv_c32.alloc(Ncs * as2.ldc32);
+                const size_t tot = Ncs * as2.ldc32;
+                as_coarse_to_f32_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
+                    as2.ainv_c.ptr, as2.Nc, as2.ldc32, as2.ainv_c32.ptr);
+            } else {
+                as2.ainv_c32.release();
+            }
             CK(cudaGetLastError());
             std::vector<int> hinfo(infos.count);
             d2h(hinfo.data(), infos.ptr, hinfo.size() * sizeof(int), stream);
@@ -946,6 +957,8 @@ struct tsv_ctx {
         a.rc = as2.rc.ptr;
         a.zc = as2.zc.ptr;
         a.ainv_c = as2.ainv_c.ptr;
+        a.ainv_c32 = as2.ainv_c32.ptr;
+        a.ldc32 = as2.ldc32;
         a.Nc = as2.Nc;
         a.round_bits = as_round_bits();
         if (as2.tc) {

@@ -37,6 +37,8 @@ struct AsParams {
     double *cellpart;      // [ncells][24]
     double *rc, *zc;       // coarse vectors [Nc]
     const double *ainv_c;  // dense [Nc][Nc]
+    const float *ainv_c32; // FP32 copy [Nc][ldc32] (default coarse solve; halves its HBM stream)
+    int ldc32;
     int Nc;
     int round_bits;        // experiment: round the local-solve operand to this many mantissa bits (0 = off)
     // tensor-core local solve (tc_local.cuh): TF32 operand panel and the
@@ -229,9 +231,22 @@ __global__ void as_coarse_gemv_kernel(CgParams q, AsParams a) {
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (row >= a.Nc) return;
-    const double *m = a.ainv_c + static_cast<long long>(row) * a.Nc;
     double s = 0.0;
-    for (int j = lane; j < a.Nc; j += 32) s += m[j] * a.rc[j];
+    if (a.ainv_c32) {
+        const float4 *m4 = reinterpret_cast<const float4 *>(a.ainv_c32 + static_cast<long long>(row) * a.ldc32);
+        const int n4 = a.Nc >> 2;
+        for (int j = lane; j < n4; j += 32) {
+            const float4 v = __ldcs(m4 + j);
+            const double *rc = a.rc + 4 * j;
+            s += static_cast<double>(v.x) * rc[0] + static_cast<double>(v.y) * rc[1] + static_cast<double>(v.z) * rc[2] +
+                 static_cast<double>(v.w) * rc[3];
+        }
+        const float *m = a.ainv_c32 + static_cast<long long>(row) * a.ldc32;
+        for (int j = 4 * n4 + lane; j < a.Nc; j += 32) s += static_cast<double>(m[j]) * a.rc[j];
+    } else {
+        const double *m = a.ainv_c + static_cast<long long>(row) * a.Nc;
+        for (int j = lane; j < a.Nc; j += 32) s += m[j] * a.rc[j];
+    }
     s = warp_sum(s);
     if (lane == 0) a.zc[row] = s;
 }
@@ -339,6 +354,14 @@ __global__ void as_fix_zero_rows_kernel(double *Ac, int Nc) {
     for (int j = lane; j < Nc && !nz; j += 32) nz = Ac[static_cast<long long>(row) * Nc + j] != 0.0;
     nz = __any_sync(0xffffffffu, nz);
     if (!nz && lane == 0) Ac[static_cast<long long>(row) * Nc + row] = 1.0;
+}
+
+// FP32 copy of the coarse inverse, rows padded to ld.
+__global__ void as_coarse_to_f32_kernel(const double *A, int Nc, int ld, float *dst) {
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<long long>(Nc) * ld) return;
+    const int row = static_cast<int>(t / ld), col = static_cast<int>(t % ld);
+    dst[t] = col < Nc ? static_cast<float>(A[static_cast<long long>(row) * Nc + col]) : 0.0f;
 }
 
 // Lower triangle -> full symmetric (column-major).
