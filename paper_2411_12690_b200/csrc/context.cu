@@ -137,6 +137,7 @@ struct tsv_ctx {
     std::vector<uint8_t> row_kind, tile_kind;
     std::vector<double> row_dt;
     std::vector<uint32_t> node_glob_of_int, node_int_of_glob;
+    std::vector<int> node_super_ptr;  // [super cell + 1] internal node ranges (super-cell-major numbering)
 
     // boundary conditions (reference numbering)
     bool bc_set = false;
@@ -164,17 +165,15 @@ struct tsv_ctx {
     struct As2 {
         int s = 0, SX = 0, SY = 0, Nc = 0, ncells = 0, ntypes = 0, step = 0;
         size_t BL_pad = 0, mtiles = 0;
-        DevBuf<int> slots2, tile_type, cell_ptr, cell_node;
+        DevBuf<int> slots2, tile_type, cell_ptr;
         DevBuf<double> XL, ZL, z, cellpart, rc, zc, ainv_c, ainv_store;
         DevBuf<const double *> ainv_tab;
         DevBuf<short4> lat;
         double setup_ms = 0.0;
         // tensor-core (TF32) local solves
         bool tc = false;
-        int KP = 0, NP = 0, BN = 0, ntn = 0;
-        DevBuf<float> XL32, ainv32;
-        DevBuf<int> slotsZ;
-        DevBuf<double> ZT;
+        int KP = 0, NP = 0, BN = 0, ntn = 0, LD = 0;  // LD: row stride of XL32 and ZL
+        DevBuf<float> XL32, ainv32, ZL32;
         CUtensorMap tmA{}, tmB{};
         DevBuf<float> ainv_c32;
         int ldc32 = 0;
@@ -268,29 +267,46 @@ struct tsv_ctx {
         k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(k1_grid);  // fewer tiles than CTA slots
         setup_streamk();
 
-        // Block-major node renumbering + slot table.
+        // Node renumbering (first visit, blocks in super-cell-major order:
+        // the nodes of each Schwarz super cell form one contiguous range)
+        // + slot table.
         const size_t nn = nl.node_count();
         node_int_of_glob.assign(nodes, 0xffffffffu);
         node_glob_of_int.clear();
         node_glob_of_int.reserve(nodes);
         std::vector<int> slot_tab(nodes * 4, -1);
-        for (size_t j = 0; j < B_pad; ++j) {
-            const int cell = row_cell[j];
-            if (cell < 0) continue;
-            const uint32_t *dm = dofmap.data() + static_cast<size_t>(cell) * n;
-            for (size_t rank = 0; rank < nn; ++rank) {
-                const uint32_t gnode = dm[3 * rank] / 3;
-                uint32_t &in = node_int_of_glob[gnode];
-                if (in == 0xffffffffu) {
-                    in = static_cast<uint32_t>(node_glob_of_int.size());
-                    node_glob_of_int.push_back(gnode);
-                }
-                int *s = slot_tab.data() + static_cast<size_t>(in) * 4;
-                int k = 0;
-                while (k < 4 && s[k] >= 0) ++k;
-                if (k == 4) throw StatusError(TSV_EINVAL, "index: a reduced node is shared by more than 4 blocks");
-                s[k] = static_cast<int>(j * ldk + rank);  // + c * nn per component
+        const uint32_t sbn = static_cast<uint32_t>(schwarz_super_block(rows, cols));
+        std::vector<int> visit;
+        visit.reserve(B);
+        node_super_ptr.assign(1, 0);
+        for (uint32_t cy = 0; cy < (rows + sbn - 1) / sbn; ++cy)
+            for (uint32_t cx = 0; cx < (cols + sbn - 1) / sbn; ++cx) {
+                for (uint32_t r = cy * sbn; r < std::min(rows, (cy + 1) * sbn); ++r)
+                    for (uint32_t c = cx * sbn; c < std::min(cols, (cx + 1) * sbn); ++c)
+                        visit.push_back(static_cast<int>(static_cast<size_t>(r) * cols + c));
+                node_super_ptr.push_back(static_cast<int>(visit.size()));  // block counts for now
             }
+        const std::vector<int> super_blocks = node_super_ptr;
+        for (size_t sc = 0; sc + 1 < super_blocks.size(); ++sc) {
+            for (int v = super_blocks[sc]; v < super_blocks[sc + 1]; ++v) {
+                const int cell = visit[v];
+                const size_t j = static_cast<size_t>(cell_row[cell]);
+                const uint32_t *dm = dofmap.data() + static_cast<size_t>(cell) * n;
+                for (size_t rank = 0; rank < nn; ++rank) {
+                    const uint32_t gnode = dm[3 * rank] / 3;
+                    uint32_t &in = node_int_of_glob[gnode];
+                    if (in == 0xffffffffu) {
+                        in = static_cast<uint32_t>(node_glob_of_int.size());
+                        node_glob_of_int.push_back(gnode);
+                    }
+                    int *s = slot_tab.data() + static_cast<size_t>(in) * 4;
+                    int k = 0;
+                    while (k < 4 && s[k] >= 0) ++k;
+                    if (k == 4) throw StatusError(TSV_EINVAL, "index: a reduced node is shared by more than 4 blocks");
+                    s[k] = static_cast<int>(j * ldk + rank);  // + c * nn per component
+                }
+            }
+            node_super_ptr[sc + 1] = static_cast<int>(node_glob_of_int.size());
         }
         if (node_glob_of_int.size() != nodes) throw StatusError(TSV_EINVAL, "index: unreferenced global node");
 
@@ -366,6 +382,19 @@ struct tsv_ctx {
         CK(cudaMemsetAsync(sk_flag.ptr, 0, G * sizeof(int), stream));
         sk_work.alloc(G * static_cast<size_t>(K1Cfg::FM * K1Cfg::FN * 2 * K1Cfg::THREADS));
         k1_streamk = true;
+    }
+
+    // Super-block side s of the Schwarz coarse space: the smallest s whose
+    // corner lattice has <= TSV_AS_COARSE_MAX (8192) coarse DoFs, or TSV_AS_S.
+    // It also fixes the node numbering (set_layout), so it depends only on
+    // the array shape.
+    static int schwarz_super_block(uint32_t rows, uint32_t cols) {
+        if (getenv("TSV_AS_S")) return std::max(1, std::atoi(getenv("TSV_AS_S")));
+        const size_t cap = getenv("TSV_AS_COARSE_MAX") ? std::strtoul(getenv("TSV_AS_COARSE_MAX"), nullptr, 10) : 8192;
+        for (int sb = 1;; ++sb) {
+            const size_t SX = (cols + sb - 1) / sb, SY = (rows + sb - 1) / sb;
+            if ((SX + 1) * (SY + 1) * 6 <= cap || (SX == 1 && SY == 1)) return sb;
+        }
     }
 
     static bool getenv_flag(const char *name) {
@@ -632,6 +661,7 @@ struct tsv_ctx {
             as2.ntn = static_cast<int>((n + 255) / 256);
             as2.BN = static_cast<int>(round_up((n + as2.ntn - 1) / as2.ntn, 16));
             as2.NP = as2.ntn * as2.BN;
+            as2.LD = std::max(as2.KP, as2.NP);
             as2.ainv32.alloc(static_cast<size_t>(T) * as2.NP * as2.KP);
             CK(cudaMemsetAsync(as2.ainv32.ptr, 0, as2.ainv32.count * sizeof(float), stream));
             as2.ainv_store.release();
@@ -666,7 +696,7 @@ struct tsv_ctx {
         tick("local inverses (device)");
         // --- 3. type-ordered panel rows (types padded to the small-GEMM tile height)
         const size_t BML = as2.tc ? static_cast<size_t>(kTcBM) : K1SmallCfg::BM;
-        const size_t lstride = as2.tc ? static_cast<size_t>(as2.KP) : ldk;
+        const size_t lstride = as2.tc ? static_cast<size_t>(as2.LD) : ldk;
         std::vector<int> rowL(B, -1), tiles;
         size_t row = 0;
         {
@@ -683,7 +713,7 @@ struct tsv_ctx {
         as2.mtiles = row / BML;
         if (as2.BL_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
         as2.tile_type.upload(tiles.data(), tiles.size(), stream);
-        std::vector<int> s2(nodes * 4, -1), sz(as2.tc ? nodes * 4 : 0, -1);
+        std::vector<int> s2(nodes * 4, -1);
         for (size_t cell = 0; cell < B; ++cell) {
             const uint32_t *dm = dofmap.data() + cell * n;
             for (size_t rank = 0; rank < nn; ++rank) {
@@ -692,17 +722,14 @@ struct tsv_ctx {
                 int k = 0;
                 while (sl[k] >= 0) ++k;
                 sl[k] = static_cast<int>(static_cast<size_t>(rowL[cell]) * lstride + rank);
-                if (as2.tc) sz[in * 4 + k] = static_cast<int>(rank * as2.BL_pad + static_cast<size_t>(rowL[cell]));
             }
         }
         as2.slots2.upload(s2.data(), s2.size(), stream);
         if (as2.tc) {
-            if (static_cast<size_t>(as2.NP) * as2.BL_pad >= 0x7fffffffULL || as2.BL_pad * as2.KP >= 0x7fffffffULL)
-                throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
-            as2.slotsZ.upload(sz.data(), sz.size(), stream);
-            as2.XL32.alloc(as2.BL_pad * as2.KP);
+            if (as2.BL_pad * as2.LD >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
+            as2.XL32.alloc(as2.BL_pad * as2.LD);
             CK(cudaMemsetAsync(as2.XL32.ptr, 0, as2.XL32.count * sizeof(float), stream));
-            as2.ZT.alloc(static_cast<size_t>(as2.NP) * as2.BL_pad);
+            as2.ZL32.alloc(as2.BL_pad * as2.LD);
             as2.XL.release();
             as2.ZL.release();
             encode_tc_maps(T);
@@ -711,19 +738,15 @@ struct tsv_ctx {
             as2.ZL.alloc(as2.BL_pad * ldk);
             CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
             as2.XL32.release();
-            as2.ZT.release();
-            as2.slotsZ.release();
+            as2.ZL32.release();
         }
         as2.z.alloc(N);
         tick("panel tables");
         // --- 4. coarse space: corners of s x s super-blocks, bottom/top planes
         const uint32_t q = nl.n_x;
-        const size_t cap = getenv("TSV_AS_COARSE_MAX") ? std::strtoul(getenv("TSV_AS_COARSE_MAX"), nullptr, 10) : 8192;
-        int sb = getenv("TSV_AS_S") ? std::max(1, std::atoi(getenv("TSV_AS_S"))) : 1;
-        for (; !getenv("TSV_AS_S"); ++sb) {
-            const size_t SX = (cols + sb - 1) / sb, SY = (rows + sb - 1) / sb;
-            if ((SX + 1) * (SY + 1) * 6 <= cap || (SX == 1 && SY == 1)) break;
-        }
+        const int sb = schwarz_super_block(rows, cols);
+        if (node_super_ptr.size() != static_cast<size_t>(((cols + sb - 1) / sb) * ((rows + sb - 1) / sb)) + 1)
+            throw StatusError(TSV_ESTATE, "schwarz2: super-block size changed since set_layout");
         as2.s = sb;
         as2.SX = static_cast<int>((cols + sb - 1) / sb);
         as2.SY = static_cast<int>((rows + sb - 1) / sb);
@@ -731,22 +754,13 @@ struct tsv_ctx {
         as2.Nc = (as2.SX + 1) * (as2.SY + 1) * 6;
         as2.ncells = as2.SX * as2.SY;
         std::vector<short4> lat(nodes);
-        std::vector<std::vector<int>> cellnodes(static_cast<size_t>(as2.ncells));
         for (size_t in = 0; in < nodes; ++in) {
             const auto &L = index.lattice_of_node[node_glob_of_int[in]];
             lat[in] = make_short4(static_cast<short>(L[0]), static_cast<short>(L[1]), static_cast<short>(L[2]), 0);
-            const int cx = std::min(static_cast<int>(L[0]) / as2.step, as2.SX - 1);
-            const int cy = std::min(static_cast<int>(L[1]) / as2.step, as2.SY - 1);
-            cellnodes[static_cast<size_t>(cy) * as2.SX + cx].push_back(static_cast<int>(in));
-        }
-        std::vector<int> cptr(1, 0), cnode;
-        for (auto &v : cellnodes) {
-            cnode.insert(cnode.end(), v.begin(), v.end());
-            cptr.push_back(static_cast<int>(cnode.size()));
         }
         as2.lat.upload(lat.data(), lat.size(), stream);
-        as2.cell_ptr.upload(cptr.data(), cptr.size(), stream);
-        as2.cell_node.upload(cnode.data(), cnode.size(), stream);
+        as2.cell_ptr.upload(node_super_ptr.data(), node_super_ptr.size(), stream);
+        if (partial.count < 2 * static_cast<size_t>(as2.ncells)) partial.alloc(2 * static_cast<size_t>(as2.ncells));
         as2.cellpart.alloc(static_cast<size_t>(as2.ncells) * 24);
         as2.rc.alloc(as2.Nc);
         as2.zc.alloc(as2.Nc);
@@ -849,7 +863,7 @@ struct tsv_ctx {
             spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, infos.ptr + 2 * T);
             as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
                                                                                                        as2.Nc);
-            if (!getenv_flag("TSV_AS_COARSE_F64")) {
+            if (getenv_flag("TSV_AS_COARSE_F32")) {
                 as2.ldc32 = static_cast<int>(round_up(Ncs, 32));
                 as2.ainv_c32.alloc(Ncs * as2.ldc32);
                 const size_t tot = Ncs * as2.ldc32;
@@ -901,9 +915,9 @@ struct tsv_ctx {
             return reinterpret_cast<EncodeFn>(fn);
         }();
         if (!encode) throw StatusError(TSV_ECUDA, "schwarz2: cuTensorMapEncodeTiled unavailable");
-        auto make = [&](CUtensorMap *m, void *ptr, uint64_t rows_, uint32_t box_rows) {
+        auto make = [&](CUtensorMap *m, void *ptr, uint64_t rows_, uint32_t box_rows, int row_stride) {
             const cuuint64_t dims[2] = {static_cast<cuuint64_t>(as2.KP), rows_};
-            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(as2.KP) * sizeof(float)};
+            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride) * sizeof(float)};
             const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTcBK), box_rows};
             const cuuint32_t estr[2] = {1, 1};
             if (encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -911,8 +925,8 @@ struct tsv_ctx {
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
                 throw StatusError(TSV_ECUDA, "schwarz2: tensor map encoding failed");
         };
-        make(&as2.tmA, as2.XL32.ptr, as2.BL_pad, static_cast<uint32_t>(kTcBM));
-        make(&as2.tmB, as2.ainv32.ptr, static_cast<uint64_t>(T) * as2.NP, static_cast<uint32_t>(as2.BN));
+        make(&as2.tmA, as2.XL32.ptr, as2.BL_pad, static_cast<uint32_t>(kTcBM), as2.LD);
+        make(&as2.tmB, as2.ainv32.ptr, static_cast<uint64_t>(T) * as2.NP, static_cast<uint32_t>(as2.BN), as2.KP);
         static bool attr = false;
         if (!attr) {
             CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
@@ -926,8 +940,8 @@ struct tsv_ctx {
         tp.NP = as2.NP;
         tp.BN = as2.BN;
         tp.k_blocks = as2.KP / kTcBK;
-        tp.ZT = as2.ZT.ptr;
-        tp.ldz = static_cast<long long>(as2.BL_pad);
+        tp.ZL = as2.ZL32.ptr;
+        tp.ldz = static_cast<long long>(as2.LD);
         tp.done = &state.ptr->done;
         tc_local_tf32_kernel<<<dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.mtiles)), kTcThreads,
                                tc_smem_bytes(as2.BN), stream>>>(as2.tmA, as2.tmB, tp);
@@ -951,7 +965,6 @@ struct tsv_ctx {
         a.lat_y = static_cast<int>(index.lat_y);
         a.qm1 = static_cast<int>(nl.n_z - 1);
         a.cell_ptr = as2.cell_ptr.ptr;
-        a.cell_node = as2.cell_node.ptr;
         a.ncells = as2.ncells;
         a.cellpart = as2.cellpart.ptr;
         a.rc = as2.rc.ptr;
@@ -963,9 +976,7 @@ struct tsv_ctx {
         a.round_bits = as_round_bits();
         if (as2.tc) {
             a.XL32 = as2.XL32.ptr;
-            a.ZT = as2.ZT.ptr;
-            a.slotsZ = as2.slotsZ.ptr;
-            a.zt_cstride = static_cast<long long>(nn_count()) * static_cast<long long>(as2.BL_pad);
+            a.ZL32 = as2.ZL32.ptr;
         }
         return a;
     }
@@ -983,8 +994,8 @@ struct tsv_ctx {
         }
         as_restrict_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
         as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, stream>>>(q, a);
-        as_coarse_gemv_kernel<<<(as2.Nc + 7) / 8, 256, 0, stream>>>(q, a);
-        as_z_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, stream>>>(q, a);
+        as_z_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
         launches += 6;
     }
 

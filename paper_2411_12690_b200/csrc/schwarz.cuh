@@ -26,27 +26,26 @@ namespace tsvb200 {
 
 struct AsParams {
     const int *slots2;     // [node][4] offsets into XL / ZL (type-ordered panel rows)
-    double *XL;            // local-solve operand panel
-    const double *ZL;      // local-solve product panel
+    double *XL;            // local-solve operand panel (FP64 path)
+    const double *ZL;      // local-solve product panel (FP64 path)
+    const float *ZL32;     // local-solve product panel (tensor-core path)
     double *z;             // [3][node] preconditioned residual
     const short4 *lat;     // (gx, gy, gz) lattice position of each internal node
     int step, SX, SY, lat_x, lat_y, qm1;
-    const int *cell_ptr;   // super cell -> range of cell_node
-    const int *cell_node;  // internal nodes grouped by super cell
+    const int *cell_ptr;   // super cell -> its contiguous internal node range
     int ncells;
     double *cellpart;      // [ncells][24]
     double *rc, *zc;       // coarse vectors [Nc]
     const double *ainv_c;  // dense [Nc][Nc]
-    const float *ainv_c32; // FP32 copy [Nc][ldc32] (default coarse solve; halves its HBM stream)
+    const float *ainv_c32; // optional FP32 copy [Nc][ldc32] (TSV_AS_COARSE_F32: halves the coarse HBM
+                           // stream, but with the TF32 local solves it multiplies the residual-check
+                           // restarts near tol 1e-12 at config 3: 124-158 vs 79-84 iterations)
     int ldc32;
     int Nc;
     int round_bits;        // experiment: round the local-solve operand to this many mantissa bits (0 = off)
-    // tensor-core local solve (tc_local.cuh): TF32 operand panel and the
-    // transposed FP64 product ZT[col][row]; slotsZ[node][4] = rank * rows + row
+    // tensor-core local solve (tc_local.cuh): TF32 operand panel (same
+    // row stride as ZL, so slots2 addresses both)
     float *XL32;
-    const double *ZT;
-    const int *slotsZ;
-    long long zt_cstride;  // nn * rows: component stride in ZT
 };
 
 // Round to `bits` explicit mantissa bits (emulates a low-precision operand).
@@ -59,18 +58,37 @@ __device__ __forceinline__ double round_mantissa(double v, int bits) {
     return __longlong_as_double(i);
 }
 
-__device__ __forceinline__ void as_cell_weights(const AsParams &a, int node, int &cx, int &cy, double w[8]) {
+// Trilinear weights of a node relative to super cell (cx, cy). Nodes are
+// numbered super-cell-major, so a CTA per super cell sees a contiguous node
+// range [cell_ptr[c], cell_ptr[c+1]) lying in that (closed) cell.
+struct AsCell {
+    int cx, cy, x0, y0;
+    double rdx, rdy, rdz;  // reciprocal cell extents (lattice units)
+};
+
+__device__ __forceinline__ AsCell as_cell(const AsParams &a, int cell) {
+    AsCell c;
+    c.cx = cell % a.SX;
+    c.cy = cell / a.SX;
+    c.x0 = c.cx * a.step;
+    c.y0 = c.cy * a.step;
+    c.rdx = 1.0 / static_cast<double>(min(c.x0 + a.step, a.lat_x - 1) - c.x0);
+    c.rdy = 1.0 / static_cast<double>(min(c.y0 + a.step, a.lat_y - 1) - c.y0);
+    c.rdz = 1.0 / static_cast<double>(a.qm1);
+    return c;
+}
+
+// Restriction (as_restrict_kernel) and prolongation (as_z_kernel) evaluate
+// the same weights for the same node (its owner cell), so the two-level
+// preconditioner stays symmetric.
+__device__ __forceinline__ void as_cell_weights(const AsParams &a, const AsCell &c, int node, double w[8]) {
     const short4 L = a.lat[node];
-    cx = min(static_cast<int>(L.x) / a.step, a.SX - 1);
-    cy = min(static_cast<int>(L.y) / a.step, a.SY - 1);
-    const int x0 = cx * a.step, x1 = min(x0 + a.step, a.lat_x - 1);
-    const int y0 = cy * a.step, y1 = min(y0 + a.step, a.lat_y - 1);
-    const double tx = static_cast<double>(L.x - x0) / static_cast<double>(x1 - x0);
-    const double ty = static_cast<double>(L.y - y0) / static_cast<double>(y1 - y0);
-    const double tz = static_cast<double>(L.z) / static_cast<double>(a.qm1);
+    const double tx = static_cast<double>(L.x - c.x0) * c.rdx;
+    const double ty = static_cast<double>(L.y - c.y0) * c.rdy;
+    const double tz = static_cast<double>(L.z) * c.rdz;
 #pragma unroll
-    for (int c = 0; c < 8; ++c)
-        w[c] = ((c & 1) ? tx : 1.0 - tx) * ((c & 2) ? ty : 1.0 - ty) * ((c & 4) ? tz : 1.0 - tz);
+    for (int k = 0; k < 8; ++k)
+        w[k] = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
 }
 
 __device__ __forceinline__ int as_corner_node(const AsParams &a, int cx, int cy, int c) {
@@ -115,13 +133,13 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
                 if (s.y >= 0) a.XL32[s.y + co] = f;
                 if (s.z >= 0) a.XL32[s.z + co] = f;
                 if (s.w >= 0) a.XL32[s.w + co] = f;
-                continue;
+            } else {
+                rv = round_mantissa(rv, a.round_bits);
+                if (s.x >= 0) a.XL[s.x + co] = rv;
+                if (s.y >= 0) a.XL[s.y + co] = rv;
+                if (s.z >= 0) a.XL[s.z + co] = rv;
+                if (s.w >= 0) a.XL[s.w + co] = rv;
             }
-            rv = round_mantissa(rv, a.round_bits);
-            if (s.x >= 0) a.XL[s.x + co] = rv;
-            if (s.y >= 0) a.XL[s.y + co] = rv;
-            if (s.z >= 0) a.XL[s.z + co] = rv;
-            if (s.w >= 0) a.XL[s.w + co] = rv;
         }
     }
     block_sum<1>(part, sh);
@@ -168,25 +186,24 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
     __threadfence();
 }
 
-// Restriction, per super cell: partial P^T r over the cell's nodes (24 values).
-__global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a) {
+// Restriction, one CTA per super cell over its contiguous node range: the
+// cell's 24 partials of P^T r.
+__global__ void __launch_bounds__(256, 3) as_restrict_kernel(CgParams q, AsParams a) {
     __shared__ double sh[8][24];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
-    const int cell = blockIdx.x;
     const int N = q.n_nodes;
+    const int cell = blockIdx.x;
+    const AsCell cc = as_cell(a, cell);
     double acc[24];
 #pragma unroll
     for (int k = 0; k < 24; ++k) acc[k] = 0.0;
-    for (int i = a.cell_ptr[cell] + threadIdx.x; i < a.cell_ptr[cell + 1]; i += blockDim.x) {
-        const int node = a.cell_node[i];
-        int cx, cy;
+    for (int node = a.cell_ptr[cell] + threadIdx.x; node < a.cell_ptr[cell + 1]; node += blockDim.x) {
         double w[8];
-        as_cell_weights(a, node, cx, cy, w);
+        as_cell_weights(a, cc, node, w);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
-            if (q.cmask[dof]) continue;
-            const double rv = q.r[dof];
+            const double rv = q.cmask[dof] ? 0.0 : q.r[dof];
 #pragma unroll
             for (int k = 0; k < 8; ++k) acc[3 * k + c] += w[k] * rv;
         }
@@ -199,9 +216,9 @@ __global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a
     }
     __syncthreads();
     if (threadIdx.x < 24) {
-        double s = 0.0;
-        for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) s += sh[w2][threadIdx.x];
-        a.cellpart[cell * 24 + threadIdx.x] = s;
+        double t = 0.0;
+        for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) t += sh[w2][threadIdx.x];
+        a.cellpart[cell * 24 + threadIdx.x] = t;
     }
 }
 
@@ -225,45 +242,72 @@ __global__ void as_coarse_rhs_kernel(CgParams q, AsParams a) {
     a.rc[j] = s;
 }
 
-// Coarse solve: zc = A_c^-1 rc, one warp per row (fixed-order reduction).
-__global__ void as_coarse_gemv_kernel(CgParams q, AsParams a) {
+// Coarse solve zc = A_c^-1 rc (fixed-order reductions): a CTA of 8 warps
+// computes 16 rows, 2 per warp, over rc chunks staged in shared memory (the
+// rows re-read rc from shared memory, not L2). FP32 matrix by default.
+constexpr int kGemvRows = 16;
+constexpr int kGemvChunk = 2048;
+
+__global__ void __launch_bounds__(256) as_coarse_gemv_kernel(CgParams q, AsParams a) {
+    __shared__ double rcs[kGemvChunk];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
-    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= a.Nc) return;
-    double s = 0.0;
-    if (a.ainv_c32) {
-        const float4 *m4 = reinterpret_cast<const float4 *>(a.ainv_c32 + static_cast<long long>(row) * a.ldc32);
-        const int n4 = a.Nc >> 2;
-        for (int j = lane; j < n4; j += 32) {
-            const float4 v = __ldcs(m4 + j);
-            const double *rc = a.rc + 4 * j;
-            s += static_cast<double>(v.x) * rc[0] + static_cast<double>(v.y) * rc[1] + static_cast<double>(v.z) * rc[2] +
-                 static_cast<double>(v.w) * rc[3];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = blockIdx.x * kGemvRows + 2 * warp;
+    const bool v0 = r0 < a.Nc, v1 = r0 + 1 < a.Nc;
+    double s0 = 0.0, s1 = 0.0;
+    for (int c0 = 0; c0 < a.Nc; c0 += kGemvChunk) {
+        const int len = min(kGemvChunk, a.Nc - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < kGemvChunk; i += blockDim.x) rcs[i] = i < len ? a.rc[c0 + i] : 0.0;
+        __syncthreads();
+        if (a.ainv_c32) {
+            const int n4 = (len + 3) >> 2;  // rows are zero-padded to ldc32
+            const float4 *m0 = reinterpret_cast<const float4 *>(a.ainv_c32 + static_cast<long long>(v0 ? r0 : 0) * a.ldc32 + c0);
+            const float4 *m1 = reinterpret_cast<const float4 *>(a.ainv_c32 + static_cast<long long>(v1 ? r0 + 1 : 0) * a.ldc32 + c0);
+            for (int j = lane; j < n4; j += 32) {
+                const float4 x0 = __ldcs(m0 + j), x1 = __ldcs(m1 + j);
+                const double4 rv = make_double4(rcs[4 * j], rcs[4 * j + 1], rcs[4 * j + 2], rcs[4 * j + 3]);
+                s0 += static_cast<double>(x0.x) * rv.x + static_cast<double>(x0.y) * rv.y + static_cast<double>(x0.z) * rv.z +
+                      static_cast<double>(x0.w) * rv.w;
+                s1 += static_cast<double>(x1.x) * rv.x + static_cast<double>(x1.y) * rv.y + static_cast<double>(x1.z) * rv.z +
+                      static_cast<double>(x1.w) * rv.w;
+            }
+        } else {
+            const double *m0 = a.ainv_c + static_cast<long long>(v0 ? r0 : 0) * a.Nc + c0;
+            const double *m1 = a.ainv_c + static_cast<long long>(v1 ? r0 + 1 : 0) * a.Nc + c0;
+            for (int j = lane; j < len; j += 32) {
+                s0 += m0[j] * rcs[j];
+                s1 += m1[j] * rcs[j];
+            }
         }
-        const float *m = a.ainv_c32 + static_cast<long long>(row) * a.ldc32;
-        for (int j = 4 * n4 + lane; j < a.Nc; j += 32) s += static_cast<double>(m[j]) * a.rc[j];
-    } else {
-        const double *m = a.ainv_c + static_cast<long long>(row) * a.Nc;
-        for (int j = lane; j < a.Nc; j += 32) s += m[j] * a.rc[j];
     }
-    s = warp_sum(s);
-    if (lane == 0) a.zc[row] = s;
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+        if (v0) a.zc[r0] = s0;
+        if (v1) a.zc[r0 + 1] = s1;
+    }
 }
 
-// Z: z = sum of local products (owner gather) + P zc; (r.z) reduced; the
-// last CTA sets beta / rho (p = z + beta p, or p = z after init/restart).
+// Z, one CTA per super cell: z = sum of local products (owner gather) +
+// P zc (the cell's 24 coarse values staged in shared memory); (r.z)
+// reduced; the last CTA sets beta / rho (p = z + beta p, or p = z after
+// init/restart).
 __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
     __shared__ double sh[64];
+    __shared__ double zc[24];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int N = q.n_nodes;
+    const int cell = blockIdx.x;
+    const AsCell cc = as_cell(a, cell);
+    if (threadIdx.x < 24) zc[threadIdx.x] = a.zc[3 * as_corner_node(a, cc.cx, cc.cy, threadIdx.x / 3) + threadIdx.x % 3];
+    __syncthreads();
     double part[1] = {0.0};
-    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
-        const int4 s = reinterpret_cast<const int4 *>(a.ZT ? a.slotsZ : a.slots2)[node];
-        int cx, cy;
+    for (int node = a.cell_ptr[cell] + threadIdx.x; node < a.cell_ptr[cell + 1]; node += blockDim.x) {
+        const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
         double w[8];
-        as_cell_weights(a, node, cx, cy, w);
+        as_cell_weights(a, cc, node, w);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
@@ -272,22 +316,21 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
             if (q.cmask[dof]) {
                 zv = rv;  // unit row of the lifted matrix
             } else {
+                const int co = c * q.nn;
                 zv = 0.0;
-                if (a.ZT) {
-                    const double *zt = a.ZT + c * a.zt_cstride;
-                    if (s.x >= 0) zv += zt[s.x];
-                    if (s.y >= 0) zv += zt[s.y];
-                    if (s.z >= 0) zv += zt[s.z];
-                    if (s.w >= 0) zv += zt[s.w];
+                if (a.ZL32) {
+                    if (s.x >= 0) zv += static_cast<double>(a.ZL32[s.x + co]);
+                    if (s.y >= 0) zv += static_cast<double>(a.ZL32[s.y + co]);
+                    if (s.z >= 0) zv += static_cast<double>(a.ZL32[s.z + co]);
+                    if (s.w >= 0) zv += static_cast<double>(a.ZL32[s.w + co]);
                 } else {
-                    const int co = c * q.nn;
                     if (s.x >= 0) zv += a.ZL[s.x + co];
                     if (s.y >= 0) zv += a.ZL[s.y + co];
                     if (s.z >= 0) zv += a.ZL[s.z + co];
                     if (s.w >= 0) zv += a.ZL[s.w + co];
                 }
 #pragma unroll
-                for (int k = 0; k < 8; ++k) zv += w[k] * a.zc[3 * as_corner_node(a, cx, cy, k) + c];
+                for (int k = 0; k < 8; ++k) zv += w[k] * zc[3 * k + c];
             }
             a.z[dof] = zv;
             part[0] += rv * zv;

@@ -1,6 +1,6 @@
 // Schwarz local solves on the 5th-generation tensor cores (tcgen05, kind::tf32).
 //
-//   ZT[col][row] = sum_k XL32[row][k] * Ainv32_type(row)[col][k]
+//   ZL[row][col] = sum_k XL32[row][k] * Ainv32_type(row)[col][k]
 //
 // The local inverses are a preconditioner, not the operator: the PCG
 // iteration (K1, residuals, dot products) stays FP64, only M^-1 r is formed
@@ -12,8 +12,8 @@
 // One CTA per (128-row type tile, BN-column tile): warp 0 lane 0 streams A/B
 // K-slices with TMA (128B swizzle) into a 4-stage mbarrier ring, warp 1
 // lane 0 issues tcgen05.mma into a TMEM accumulator (128 lanes x BN fp32
-// columns), and all four warps drain TMEM with tcgen05.ld into the
-// transposed output ZT (coalesced along rows).
+// columns), and all four warps drain TMEM with tcgen05.ld: each thread owns
+// one row and stores 16 consecutive FP32 columns (64 contiguous bytes).
 #pragma once
 
 #include <cuda.h>
@@ -36,8 +36,8 @@ struct TcLocalParams {
     int NP;                // rows of each type's B block (n padded to a multiple of BN)
     int BN;                // UMMA_N (multiple of 16, <= 256)
     int k_blocks;          // KP / 32
-    double *ZT;            // [NP][ldz] output, transposed
-    long long ldz;         // = panel rows
+    float *ZL;             // [rows][ldz] output (row-major, FP32 = the accumulator)
+    long long ldz;
     const int *done;       // CG state: skip the work once converged
 };
 
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     mbar_wait(smem_u32(&accum_bar), 0u);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const long long row = static_cast<long long>(m_tile) * kTcBM + warp * 32 + lane;
-    double *out = p.ZT + static_cast<long long>(n_tile) * BN * p.ldz + row;
+    float *out = p.ZL + row * p.ldz + static_cast<long long>(n_tile) * BN;
     for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t v[16];
         const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0);
@@ -180,8 +180,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint4 *o4 = reinterpret_cast<uint4 *>(out + c0);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) out[static_cast<long long>(c0 + j) * p.ldz] = static_cast<double>(__uint_as_float(v[j]));
+        for (int j = 0; j < 4; ++j) o4[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

@@ -16,7 +16,7 @@ for ci in [int(a) for a in sys.argv[1:]] or [3]:
         s1 = g.solve_global(IterOptions(1e-12, 100000, pc))
         t1 = time.perf_counter() - t
         s2 = g.solve_global(IterOptions(1e-12, 100000, pc))
-        out[pc] = dict(iterations=s2.iterations, relres=s2.relative_residual, solve_ms=round(s2.solve_ms, 2),
+        out[pc] = dict(iterations=s2.iterations, restarts=s2.restarts, relres=s2.relative_residual, solve_ms=round(s2.solve_ms, 2),
                        first_call_s=round(t1, 3), per_it_ms=round(s2.loop_ms / max(1, s2.iterations), 4))
         out[pc + "_u"] = s2.u
     if "diagonal" in out:
