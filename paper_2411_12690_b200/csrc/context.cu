@@ -1248,7 +1248,11 @@ struct tsv_ctx {
         sp.out = out;
         sp.out_cell0 = static_cast<long long>(c0);
         sp.out_cells = static_cast<long long>(c1 - c0);
-        const size_t smem = 2 * (m.cells[0] + 1) * (m.cells[1] + 1) * 3 * sizeof(double);
+        const size_t smem = (((2 * (m.cells[0] + 1) * (m.cells[1] + 1) * 3 + 1) & ~size_t(1)) + kStressThreads * 7) * sizeof(double);
+        if (points > 0 && smem > 48 * 1024) {
+            if (smem > 227 * 1024) throw StatusError(TSV_EINVAL, "recover: element layer too large for shared memory");
+            CK(cudaFuncSetAttribute(stress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        }
         size_t t = 0;
         while (t < m_tiles) {
             if (!need[t]) { ++t; continue; }
@@ -1278,7 +1282,7 @@ struct tsv_ctx {
                 sp.U = U.ptr;
                 sp.j0 = static_cast<int>(t * kBM);
                 dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>(m.cells[2]));
-                stress_kernel<<<grid, 256, smem, stream>>>(sp);
+                stress_kernel<<<grid, kStressThreads, smem, stream>>>(sp);
             } else {
                 const int res = -points;
                 CutParams cp{};

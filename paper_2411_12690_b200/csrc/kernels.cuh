@@ -673,8 +673,15 @@ struct StressParams {
     long long out_cells;      // cells in the output range
 };
 
-__global__ void stress_kernel(StressParams sp) {
-    extern __shared__ double su[];  // two node layers: 2 * nxy * 3
+// One CTA per (block, element layer). The two node layers of u are staged
+// in shared memory; points are processed in tiles of blockDim.x (one per
+// thread); each tile's 7-value records are staged in shared memory and
+// written out as contiguous 16-byte streaming stores (the layer's output is
+// one contiguous range of out).
+constexpr int kStressThreads = 256;
+
+__global__ void __launch_bounds__(kStressThreads) stress_kernel(StressParams sp) {
+    extern __shared__ double su[];  // two node layers: 2 * nxy * 3, then the output tile
     const int jr = blockIdx.x;       // row within chunk
     const int k = blockIdx.y;        // element layer
     const int j = sp.j0 + jr;
@@ -686,6 +693,7 @@ __global__ void stress_kernel(StressParams sp) {
     const int nx = sp.cx + 1, ny = sp.cy + 1, nxy = nx * ny;
     const double *U = sp.U + static_cast<long long>(jr) * sp.ldu + static_cast<long long>(k) * nxy * 3;
     for (int i = threadIdx.x; i < 2 * nxy * 3; i += blockDim.x) su[i] = U[i];
+    double *tile = su + ((2 * nxy * 3 + 1) & ~1);  // 16-byte aligned
     __syncthreads();
     const double dt = sp.row_dt[j];
     const double *hx = sp.hinv[kind], *hy = hx + sp.cx, *hz = hy + sp.cy;
@@ -694,54 +702,72 @@ __global__ void stress_kernel(StressParams sp) {
     const int per_layer = sp.cx * sp.cy * P;
     const long long E = static_cast<long long>(sp.cx) * sp.cy * sp.cz;
     const double g = 0.57735026918962576451;  // 1/sqrt(3)
-    double *out_cell = sp.out + oc * E * P * 7;
-    for (int t = threadIdx.x; t < per_layer; t += blockDim.x) {
-        const int gp = t % P, e2 = t / P;
-        const int i = e2 % sp.cx, jj = e2 / sp.cx;
-        const long long e = (static_cast<long long>(k) * sp.cy + jj) * sp.cx + i;
-        double xi = 0.0, eta = 0.0, zeta = 0.0;
-        if (P == 8) {
-            xi = (gp >> 2) ? g : -g;
-            eta = ((gp >> 1) & 1) ? g : -g;
-            zeta = (gp & 1) ? g : -g;
-        }
-        const double hxi = hx[i], hyi = hy[jj];
-        double du[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-            const int di = (a == 1 || a == 2 || a == 5 || a == 6);
-            const int dj = (a == 2 || a == 3 || a == 6 || a == 7);
-            const int dk = a >= 4;
-            const double sx = di ? 1.0 : -1.0, sy = dj ? 1.0 : -1.0, sz = dk ? 1.0 : -1.0;
-            // grad N_a = J^-1 dN/dxi with J = diag(h/2) for box cells (fem.cpp:27-58)
-            const double gxa = 0.25 * sx * (1.0 + sy * eta) * (1.0 + sz * zeta) * hxi;
-            const double gya = 0.25 * sy * (1.0 + sx * xi) * (1.0 + sz * zeta) * hyi;
-            const double gza = 0.25 * sz * (1.0 + sx * xi) * (1.0 + sy * eta) * hzi;
-            const double *ua = su + (dk * nxy + (jj + dj) * nx + (i + di)) * 3;
+    double *out_layer = sp.out + (oc * E + static_cast<long long>(k) * sp.cx * sp.cy) * P * 7;
+    for (int t0 = 0; t0 < per_layer; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        if (t < per_layer) {
+            const int gp = t % P, e2 = t / P;
+            const int i = e2 % sp.cx, jj = e2 / sp.cx;
+            const long long e = (static_cast<long long>(k) * sp.cy + jj) * sp.cx + i;
+            double xi = 0.0, eta = 0.0, zeta = 0.0;
+            if (P == 8) {
+                xi = (gp >> 2) ? g : -g;
+                eta = ((gp >> 1) & 1) ? g : -g;
+                zeta = (gp & 1) ? g : -g;
+            }
+            const double hxi = hx[i], hyi = hy[jj];
+            // grad N_a = J^-1 dN/dxi with J = diag(h/2) for box cells (fem.cpp:27-58), summed
+            // separably: d/dx = hx/4 sum_{dj,dk} (1 +- eta)(1 +- zeta) (u[1,dj,dk] - u[0,dj,dk]), etc.
+            const double ex0 = 1.0 - xi, ex1 = 1.0 + xi, ey0 = 1.0 - eta, ey1 = 1.0 + eta;
+            const double ez0 = 1.0 - zeta, ez1 = 1.0 + zeta;
+            const double qx = 0.25 * hxi, qy = 0.25 * hyi, qz = 0.25 * hzi;
+            const double *u000 = su + (jj * nx + i) * 3, *u100 = u000 + 3, *u010 = u000 + nx * 3, *u110 = u010 + 3;
+            const double *u001 = u000 + nxy * 3, *u101 = u001 + 3, *u011 = u001 + nx * 3, *u111 = u011 + 3;
+            double du[3][3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                du[c][0] += ua[c] * gxa;
-                du[c][1] += ua[c] * gya;
-                du[c][2] += ua[c] * gza;
+                const double v000 = u000[c], v100 = u100[c], v010 = u010[c], v110 = u110[c];
+                const double v001 = u001[c], v101 = u101[c], v011 = u011[c], v111 = u111[c];
+                du[c][0] = qx * (ez0 * (ey0 * (v100 - v000) + ey1 * (v110 - v010)) +
+                                 ez1 * (ey0 * (v101 - v001) + ey1 * (v111 - v011)));
+                du[c][1] = qy * (ez0 * (ex0 * (v010 - v000) + ex1 * (v110 - v100)) +
+                                 ez1 * (ex0 * (v011 - v001) + ex1 * (v111 - v101)));
+                du[c][2] = qz * (ey0 * (ex0 * (v001 - v000) + ex1 * (v101 - v100)) +
+                                 ey1 * (ex0 * (v011 - v010) + ex1 * (v111 - v110)));
             }
+            const int mat = sp.elem_mat[kind][e];
+            const double lambda = sp.lame[kind][mat][0], mu = sp.lame[kind][mat][1];
+            const double thermal = sp.lame[kind][mat][2] * dt;
+            const double exx = du[0][0], eyy = du[1][1], ezz = du[2][2];
+            const double exy = 0.5 * (du[0][1] + du[1][0]);
+            const double eyz = 0.5 * (du[1][2] + du[2][1]);
+            const double ezx = 0.5 * (du[2][0] + du[0][2]);
+            const double tr = exx + eyy + ezz;
+            const double sxx = lambda * tr + 2.0 * mu * exx - thermal;
+            const double syy = lambda * tr + 2.0 * mu * eyy - thermal;
+            const double szz = lambda * tr + 2.0 * mu * ezz - thermal;
+            const double sxy = 2.0 * mu * exy, syz = 2.0 * mu * eyz, szx = 2.0 * mu * ezx;
+            const double d1 = sxx - syy, d2 = syy - szz, d3 = szz - sxx;
+            const double vm2 = 0.5 * (d1 * d1 + d2 * d2 + d3 * d3) + 3.0 * (sxy * sxy + syz * syz + szx * szx);
+            double *o = tile + threadIdx.x * 7;
+            o[0] = sxx; o[1] = syy; o[2] = szz; o[3] = sxy; o[4] = syz; o[5] = szx;
+            o[6] = sqrt(fmax(vm2, 0.0));
         }
-        const int mat = sp.elem_mat[kind][e];
-        const double lambda = sp.lame[kind][mat][0], mu = sp.lame[kind][mat][1];
-        const double thermal = sp.lame[kind][mat][2] * dt;
-        const double exx = du[0][0], eyy = du[1][1], ezz = du[2][2];
-        const double exy = 0.5 * (du[0][1] + du[1][0]);
-        const double eyz = 0.5 * (du[1][2] + du[2][1]);
-        const double ezx = 0.5 * (du[2][0] + du[0][2]);
-        const double tr = exx + eyy + ezz;
-        const double sxx = lambda * tr + 2.0 * mu * exx - thermal;
-        const double syy = lambda * tr + 2.0 * mu * eyy - thermal;
-        const double szz = lambda * tr + 2.0 * mu * ezz - thermal;
-        const double sxy = 2.0 * mu * exy, syz = 2.0 * mu * eyz, szx = 2.0 * mu * ezx;
-        const double d1 = sxx - syy, d2 = syy - szz, d3 = szz - sxx;
-        const double vm2 = 0.5 * (d1 * d1 + d2 * d2 + d3 * d3) + 3.0 * (sxy * sxy + syz * syz + szx * szx);
-        double *o = out_cell + (e * P + gp) * 7;
-        o[0] = sxx; o[1] = syy; o[2] = szz; o[3] = sxy; o[4] = syz; o[5] = szx;
-        o[6] = sqrt(fmax(vm2, 0.0));
+        __syncthreads();
+        // the tile's records are out_layer[t0*7 .. (t0+cnt)*7): contiguous
+        const int cnt = min(static_cast<int>(blockDim.x), per_layer - t0);
+        double *dst = out_layer + static_cast<long long>(t0) * 7;
+        const int nd = cnt * 7;
+        if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            const int n2 = nd >> 1;
+            const double2 *src2 = reinterpret_cast<const double2 *>(tile);
+            double2 *dst2 = reinterpret_cast<double2 *>(dst);
+            for (int q = threadIdx.x; q < n2; q += blockDim.x) __stcs(dst2 + q, src2[q]);
+            if ((nd & 1) && threadIdx.x == 0) __stcs(dst + nd - 1, tile[nd - 1]);
+        } else {
+            for (int q = threadIdx.x; q < nd; q += blockDim.x) __stcs(dst + q, tile[q]);
+        }
+        __syncthreads();
     }
 }
 
