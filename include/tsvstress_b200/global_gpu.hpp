@@ -161,6 +161,42 @@ public:
         return sol;
     }
 
+    /// The same solve with a preconditioner outside linalg::Precond, e.g.
+    /// TSV_PRECOND_SCHWARZ2 (two-level additive Schwarz; same u within the
+    /// parity bar, far fewer iterations).
+    template <class Opts = IterOptions>
+    GlobalSolution solve_global(const Opts &o, int precond_override) {
+        tsv_iter_options c{o.tolerance, o.max_iterations, precond_override};
+        GlobalSolution sol;
+        sol.u.resize(dof_count());
+        tsv_solve_info info{};
+        const int rc = tsv_solve(ctx_, &c, sol.u.data(), &info);
+        sol.iterations = info.iterations;
+        sol.relative_residual = info.relative_residual;
+        sol.device_ms = info.solve_ms;
+        if (rc == TSV_ENOCONV) throw NoConvergence(std::move(sol), tsv_last_error(ctx_));
+        check(rc);
+        return sol;
+    }
+
+    /// rom::load_rom (rom.cpp:305-377) straight into a RomSet slot (-1 = the
+    /// file's kind); returns the kind stored in the file.
+    int load_rom_file(const std::string &path, int slot = -1) {
+        int kind = -1;
+        char err[512];
+        const int rc = tsv_load_rom_file(ctx_, slot, path.c_str(), &kind, err, sizeof err);
+        if (rc != TSV_OK) throw Error(err);
+        return kind;
+    }
+
+    /// cutplane_von_mises (global_stage.cpp:245-274) on the GPU: the
+    /// StressGrid values, [((row * cols + col) * res + py) * res + px].
+    std::vector<double> cutplane_von_mises(uint32_t res) {
+        std::vector<double> v(static_cast<size_t>(rows_) * cols_ * res * res);
+        check(tsv_cutplane(ctx_, res, v.data()));
+        return v;
+    }
+
     void set_solution(const std::vector<double> &u) { check(tsv_set_solution(ctx_, u.data())); }
 
     /// Stress + von Mises at Gauss points (points = 8) or centroids (1) of

@@ -16,6 +16,7 @@
 #include "tsvstress/linalg.hpp"
 #include "tsvstress/mesh.hpp"
 #include "tsvstress/rom.hpp"
+#include "tsvstress/stress_grid.hpp"
 #include "tsvstress_b200/global_gpu.hpp"
 
 using namespace tsvstress;
@@ -107,7 +108,28 @@ int main() {
         }
         worst = std::max(worst, dmax / vmax);
     }
-    std::printf("{\"du_rel_l2\": %.3e, \"iterations_ref\": %d, \"iterations_gpu\": %d, \"vm_rel_err\": %.3e}\n", du,
-                ref.iterations, sol.iterations, worst);
-    return (du <= 1e-10 && worst <= 1e-8) ? 0 : 1;
+    // cut plane (cutplane_von_mises, global_stage.cpp:245-274) from the same u
+    const std::uint32_t res = 20;
+    StressGrid cut_ref = global::cutplane_von_mises(ref, layout, roms, index, meshes, res, 4);
+    std::vector<double> cut_gpu = gpu.cutplane_von_mises(res);
+    double cmax = 0.0, cdiff = 0.0;
+    for (std::size_t i = 0; i < cut_gpu.size(); ++i) {
+        cmax = std::max(cmax, std::abs(cut_ref.values[i]));
+        cdiff = std::max(cdiff, std::abs(cut_ref.values[i] - cut_gpu[i]));
+    }
+
+    // the same objects with the two-level Schwarz preconditioner (TSV_PRECOND_SCHWARZ2)
+    b200::GlobalSolution sw = gpu.solve_global(opts, TSV_PRECOND_SCHWARZ2);
+    double num2 = 0.0;
+    for (std::size_t i = 0; i < ref.u.size(); ++i) num2 += (sw.u[i] - ref.u[i]) * (sw.u[i] - ref.u[i]);
+    const double du_sw = std::sqrt(num2 / den);
+
+    std::printf(
+        "{\"du_rel_l2\": %.3e, \"iterations_ref\": %d, \"iterations_gpu\": %d, \"vm_rel_err\": %.3e, "
+        "\"cutplane_rel_err\": %.3e, \"du_rel_l2_schwarz2\": %.3e, \"iterations_schwarz2\": %d}\n",
+        du, ref.iterations, sol.iterations, worst, cdiff / cmax, du_sw, sw.iterations);
+    return (du <= 1e-10 && worst <= 1e-8 && cut_gpu.size() == cut_ref.values.size() && cdiff <= 1e-8 * cmax &&
+            du_sw <= 1e-10)
+               ? 0
+               : 1;
 }

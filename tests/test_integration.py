@@ -29,3 +29,6 @@ def test_reference_objects_drive_the_gpu_stage(oracle_libs, native_lib):
     assert out.returncode == 0, out.stdout + out.stderr
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["du_rel_l2"] <= 1e-10 and r["vm_rel_err"] <= 1e-8
+    assert r["cutplane_rel_err"] <= 1e-8                       # GPU cut plane vs cutplane_von_mises
+    assert r["du_rel_l2_schwarz2"] <= 1e-10                    # two-level Schwarz through the C++ layer
+    assert r["iterations_schwarz2"] < r["iterations_ref"]
