@@ -29,6 +29,7 @@
 #include "host_index.hpp"
 #include "kernels.cuh"
 #include "schwarz.cuh"
+#include "ozaki.cuh"
 
 #include <cublas_v2.h>
 #include <cusolverDn.h>
@@ -113,6 +114,10 @@ struct RomHost {
     uint8_t fingerprint[32] = {};
     DevBuf<double> d_k, d_phi, d_ut, d_hinv, d_grid[3];
     DevBuf<uint8_t> d_em;
+    // Ozaki digit planes of K_r (int8 K1): [S][rows][KA], row exponents
+    int oz_s = 0;
+    DevBuf<int8_t> oz_b;
+    DevBuf<int> oz_eb;
 };
 
 }  // namespace
@@ -178,6 +183,13 @@ struct tsv_ctx {
         DevBuf<float> ainv_c32;
         int ldc32 = 0;
     } as2;
+    // int8 (Ozaki) K1: digit planes of the X panel
+    int oz_s = 0;            // digits per value (0 = DMMA K1)
+    int graph_oz_s = 0;      // K1 variant baked into the captured graph
+    long long oz_brows = 0;  // K rows padded to the N tiles
+    DevBuf<int8_t> oz_a;
+    DevBuf<int> oz_ea;
+    CUtensorMap oz_tmA{}, oz_tmB[2]{};
     bool sk_resident = false;
     DevBuf<int> sk_start, sk_flag;
     DevBuf<double> sk_work;
@@ -313,6 +325,7 @@ struct tsv_ctx {
         drop_graph();
         solution_valid = false;
         pre_kind = -1;
+        oz_s = 0;
         stress.release();
         cudaStream_t s = stream;
         slots.upload(slot_tab.data(), slot_tab.size(), s);
@@ -1033,8 +1046,132 @@ struct tsv_ctx {
         return gp;
     }
 
+    // ------------------------------------------------ int8 (Ozaki) K1
+    // K1 variants. Default: FP64 DMMA for every product, except that with the
+    // Schwarz preconditioner the A x of the true-residual check runs on the
+    // int8 tensor cores with 10 Ozaki digits (exact int32 accumulation: a more
+    // accurate residual, so fewer spurious restarts at tol 1e-12; config 3:
+    // 72 iterations / 1 restart instead of 84 / 5).
+    //   TSV_K1_VERIFY=0|9|10  hybrid off / digits (any preconditioner)
+    //   TSV_K1_OZAKI=9|10     every K1 on the int8 tensor cores
+    int oz_verify_digits() const {
+        if (const char *v = getenv("TSV_K1_VERIFY")) {
+            const int s = std::atoi(v);
+            return (s == 9 || s == 10) ? s : 0;
+        }
+        return pre_kind == TSV_PRECOND_SCHWARZ2 ? 10 : 0;
+    }
+
+    int oz_digits_env() const {
+        if (const int v = oz_verify_digits()) return v;
+        const char *v = getenv("TSV_K1_OZAKI");
+        if (!v) return 0;
+        const int s = std::atoi(v);
+        return (s == 9 || s == 10) ? s : 0;
+    }
+
+    template <int S>
+    void oz_prepare() {
+        constexpr int BN = OzCfg<S>::BN;
+        const int KA = static_cast<int>(ldk);
+        oz_brows = static_cast<long long>(round_up(n, BN));
+        for (int k = 0; k < 2; ++k) {
+            RomHost &m = rom[k];
+            if (!m.set || m.oz_s == S) continue;
+            m.oz_b.alloc(static_cast<size_t>(S) * oz_brows * KA);
+            m.oz_eb.alloc(static_cast<size_t>(oz_brows));
+            CK(cudaMemsetAsync(m.oz_b.ptr, 0, m.oz_b.count, stream));
+            CK(cudaMemsetAsync(m.oz_eb.ptr, 0, m.oz_eb.count * sizeof(int), stream));
+            oz_slice_kernel<S><<<static_cast<unsigned>((n + 7) / 8), 256, 0, stream>>>(
+                m.d_k.ptr, static_cast<long long>(ldk), static_cast<int>(n), static_cast<int>(ldk), m.oz_b.ptr, oz_brows, KA,
+                m.oz_eb.ptr, nullptr, nullptr);
+            CK(cudaGetLastError());
+            m.oz_s = S;
+        }
+        oz_a.alloc(static_cast<size_t>(S) * B_pad * KA);
+        oz_ea.alloc(B_pad);
+        using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            throw StatusError(TSV_ECUDA, "ozaki: cuTensorMapEncodeTiled unavailable");
+        EncodeFn encode = reinterpret_cast<EncodeFn>(fn);
+        auto make = [&](CUtensorMap *map, void *ptr, uint64_t rows_, uint32_t box_rows) {
+            const cuuint64_t dims[2] = {static_cast<cuuint64_t>(KA), rows_};
+            const cuuint64_t strides[1] = {static_cast<cuuint64_t>(KA)};
+            const cuuint32_t box[2] = {static_cast<cuuint32_t>(kOzBK), box_rows};
+            const cuuint32_t estr[2] = {1, 1};
+            if (encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                throw StatusError(TSV_ECUDA, "ozaki: tensor map encoding failed");
+        };
+        make(&oz_tmA, oz_a.ptr, static_cast<uint64_t>(S) * B_pad, static_cast<uint32_t>(kTcBM));
+        for (int k = 0; k < 2; ++k) {
+            const RomHost &m = rom[k].set ? rom[k] : rom[1 - k];
+            make(&oz_tmB[k], m.oz_b.ptr, static_cast<uint64_t>(S) * oz_brows, static_cast<uint32_t>(BN));
+        }
+        static bool attr[2] = {false, false};
+        if (!attr[S - 9]) {
+            CK(cudaFuncSetAttribute(oz_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes<S>()));
+            attr[S - 9] = true;
+        }
+        oz_s = S;
+    }
+
+    void oz_ensure() {
+        const int S = ldk <= 1024 ? oz_digits_env() : 0;  // the digit split keeps a row in registers
+        if (S == oz_s && (S == 0 || oz_a.ptr)) return;
+        if (S == 0) {
+            oz_s = 0;
+            return;
+        }
+        if (S == 10) oz_prepare<10>();
+        else oz_prepare<9>();
+    }
+
+    template <int S>
+    void launch_k1_oz(const int *done, const int *run_flag = nullptr) {
+        constexpr int BN = OzCfg<S>::BN;
+        const int KA = static_cast<int>(ldk);
+        oz_slice_kernel<S><<<static_cast<unsigned>(std::min<size_t>((B_pad + 7) / 8, static_cast<size_t>(sm_count) * 8)), 256, 0, stream>>>(
+            X.ptr, static_cast<long long>(ldk), static_cast<int>(B_pad), static_cast<int>(ldk), oz_a.ptr,
+            static_cast<long long>(B_pad), KA, oz_ea.ptr, done, run_flag);
+        OzParams op{};
+        op.tile_kind = tile_kind_d.ptr;
+        op.a_plane_rows = static_cast<long long>(B_pad);
+        op.b_plane_rows = oz_brows;
+        op.k_blocks = (KA + kOzBK - 1) / kOzBK;
+        op.ex_a = oz_ea.ptr;
+        op.ex_b[0] = (rom[0].set ? rom[0] : rom[1]).oz_eb.ptr;
+        op.ex_b[1] = (rom[1].set ? rom[1] : rom[0]).oz_eb.ptr;
+        op.C = Y.ptr;
+        op.ldc = static_cast<long long>(ldk);
+        op.n_store = static_cast<int>(n);
+        op.done = done;
+        op.run_flag = run_flag;
+        op.m_tiles = static_cast<int>(m_tiles);
+        op.n_tiles = static_cast<int>(oz_brows / BN);
+        const int tiles = op.m_tiles * op.n_tiles;
+        oz_gemm_kernel<S><<<static_cast<unsigned>(std::min(tiles, sm_count)), kTcThreads, oz_smem_bytes<S>(), stream>>>(
+            oz_tmA, oz_tmB[0], oz_tmB[1], op);
+        launches += 2;
+        CK(cudaGetLastError());
+    }
+
     void launch_k1(const int *done) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(stream, &cs));
+        if (cs == cudaStreamCaptureStatusNone) oz_ensure();
+        const int *yx = done ? &state.ptr->y_holds_x : nullptr;
+        const bool verify_mode = oz_s && oz_verify_digits();
+        const bool hybrid = verify_mode && done;
+        if (oz_s && !verify_mode) return oz_s == 9 ? launch_k1_oz<9>(done) : launch_k1_oz<10>(done);
         GemmParams gp = k1_params(done);
+        if (hybrid) gp.skip_flag = yx;
         if (k1_small) {
             gp.m_tiles = static_cast<int>(B_pad / K1SmallCfg::BM);
             gp.n_tiles = static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
@@ -1049,6 +1186,10 @@ struct tsv_ctx {
         }
         ++launches;
         CK(cudaGetLastError());
+        if (hybrid) {
+            if (oz_s == 9) launch_k1_oz<9>(done, yx);
+            else launch_k1_oz<10>(done, yx);
+        }
     }
 
     CgParams cg_params() {
@@ -1085,10 +1226,15 @@ struct tsv_ctx {
         launches += 2;
     }
 
-    int graph_kernels_per_iteration() const { return pre_kind == TSV_PRECOND_SCHWARZ2 ? 9 : 4; }
+    int graph_kernels_per_iteration() const {
+        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? 9 : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
+    }
 
     void ensure_graph() {
-        if (iter_graph) return;
+        oz_ensure();
+        if (iter_graph && graph_oz_s == oz_s) return;
+        drop_graph();
+        graph_oz_s = oz_s;
         CgParams q = cg_params();
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
@@ -1532,6 +1678,7 @@ int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
                 for (size_t k = 0; k < n; ++k) kp[pidx(a, nn) * ldk + pidx(k, nn)] = d->a_element[a * n + k];
             m.d_k.upload(kp.data(), kp.size(), ctx->stream);
             CK(cudaStreamSynchronize(ctx->stream));
+            m.oz_s = 0;  // int8 digit planes are rebuilt on next use
         }
         {
             const size_t rows = round_up(n_fine, kBN);
