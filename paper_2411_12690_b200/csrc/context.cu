@@ -142,7 +142,8 @@ struct tsv_ctx {
     std::vector<uint8_t> row_kind, tile_kind;
     std::vector<double> row_dt;
     std::vector<uint32_t> node_glob_of_int, node_int_of_glob;
-    std::vector<int> node_super_ptr;  // [super cell + 1] internal node ranges (super-cell-major numbering)
+    std::vector<int> node_super_ptr;
+    bool rhs_dirty = true;  // [super cell + 1] internal node ranges (super-cell-major numbering)
 
     // boundary conditions (reference numbering)
     bool bc_set = false;
@@ -429,7 +430,13 @@ struct tsv_ctx {
         bc_set = true;
         pre_kind = -1;
         solution_valid = false;
+        rhs_dirty = true;  // assembled on first use (set_layout + set_bc assemble it once)
+    }
+
+    void ensure_rhs() {
+        if (!rhs_dirty) return;
         build_rhs();
+        rhs_dirty = false;
     }
 
     template <typename T>
@@ -588,174 +595,12 @@ struct tsv_ctx {
                 std::fprintf(stderr, "[schwarz2] %-28s %8.1f ms\n", what,
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         };
-        // --- 1. neighbourhood types: own kind, the 4 edge neighbours' kinds
-        // (or absence), corner neighbours' presence, constrained pattern.
-        // Blocks of one type share the representative's local matrix
-        // (exact except for corner-neighbour kinds; TSV_AS_EXACT_TYPES=1
-        // makes corner kinds part of the type too).
-        tick("handles");
-        const bool exact_types = getenv_flag("TSV_AS_EXACT_TYPES");
-        std::map<std::vector<int>, int> sig_type;
-        std::vector<int> type_of(B), rep_of;
-        for (uint32_t r = 0; r < rows; ++r)
-            for (uint32_t c = 0; c < cols; ++c) {
-                const size_t cell = static_cast<size_t>(r) * cols + c;
-                std::vector<int> sig;
-                sig.push_back(layout.kind_at(cell));
-                for (int dr = -1; dr <= 1; ++dr)
-                    for (int dc = -1; dc <= 1; ++dc) {
-                        if (!dr && !dc) continue;
-                        const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
-                        const bool in = rr >= 0 && cc >= 0 && rr < rows && cc < cols;
-                        const int kd = in ? layout.kind_at(static_cast<size_t>(rr) * cols + static_cast<size_t>(cc)) : -1;
-                        sig.push_back((dr && dc && !exact_types) ? (in ? 0 : -1) : kd);
-                    }
-                const uint32_t *dm = dofmap.data() + cell * n;
-                for (size_t a = 0; a < n; ++a)
-                    if (constrained[dm[a]]) sig.push_back(1000 + static_cast<int>(a));
-                auto it = sig_type.find(sig);
-                if (it == sig_type.end()) {
-                    it = sig_type.emplace(sig, static_cast<int>(rep_of.size())).first;
-                    rep_of.push_back(static_cast<int>(cell));
-                }
-                type_of[cell] = it->second;
-            }
-        const int T = static_cast<int>(rep_of.size());
-        as2.ntypes = T;
-        tick("types");
-        // --- 2. local matrices A_b = R_b A R_b^T (lifted), assembled on host
-        // threads, inverted in place on the device, packed by a kernel.
-        std::vector<double> Aall(static_cast<size_t>(T) * n * n, 0.0);
-        {
-            const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), static_cast<unsigned>(T)));
-            std::vector<std::thread> pool;
-            for (unsigned w = 0; w < nt; ++w)
-                pool.emplace_back([&, w] {
-                    std::vector<int> idx(n);
-                    for (int t = static_cast<int>(w); t < T; t += static_cast<int>(nt)) {
-                        double *A = Aall.data() + static_cast<size_t>(t) * n * n;  // column-major
-                        const size_t cell = static_cast<size_t>(rep_of[t]);
-                        const uint32_t r = static_cast<uint32_t>(cell / cols), c = static_cast<uint32_t>(cell % cols);
-                        const uint32_t *dm = dofmap.data() + cell * n;
-                        std::unordered_map<uint32_t, int> loc;
-                        loc.reserve(2 * n);
-                        for (size_t a = 0; a < n; ++a) loc[dm[a]] = static_cast<int>(a);
-                        for (int dr = -1; dr <= 1; ++dr)
-                            for (int dc = -1; dc <= 1; ++dc) {
-                                const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
-                                if (rr < 0 || cc < 0 || rr >= rows || cc >= cols) continue;
-                                const size_t b2 = static_cast<size_t>(rr) * cols + static_cast<size_t>(cc);
-                                const uint32_t *dm2 = dofmap.data() + b2 * n;
-                                const std::vector<double> &K2 = rom[layout.kind_at(b2)].k_r;
-                                for (size_t a = 0; a < n; ++a) {
-                                    auto f = loc.find(dm2[a]);
-                                    idx[a] = f == loc.end() ? -1 : f->second;
-                                }
-                                for (size_t a = 0; a < n; ++a) {
-                                    if (idx[a] < 0) continue;
-                                    for (size_t q2 = 0; q2 < n; ++q2)
-                                        if (idx[q2] >= 0) A[static_cast<size_t>(idx[q2]) * n + idx[a]] += K2[a * n + q2];
-                                }
-                            }
-                        for (size_t a = 0; a < n; ++a)
-                            if (constrained[dm[a]]) {
-                                for (size_t k = 0; k < n; ++k) A[a * n + k] = A[k * n + a] = 0.0;
-                                A[a * n + a] = 1.0;
-                            }
-                    }
-                });
-            for (auto &th : pool) th.join();
-        }
-        tick("local assembly (host)");
-        as2.tc = !getenv_flag("TSV_AS_LOCAL_F64") && as_round_bits() == 0;
-        const size_t rowsK = round_up(n, kBN);
-        if (as2.tc) {
-            as2.KP = static_cast<int>(round_up(n, kTcBK));
-            as2.ntn = static_cast<int>((n + 255) / 256);
-            as2.BN = static_cast<int>(round_up((n + as2.ntn - 1) / as2.ntn, 16));
-            as2.NP = as2.ntn * as2.BN;
-            as2.LD = std::max(as2.KP, as2.NP);
-            as2.ainv32.alloc(static_cast<size_t>(T) * as2.NP * as2.KP);
-            CK(cudaMemsetAsync(as2.ainv32.ptr, 0, as2.ainv32.count * sizeof(float), stream));
-            as2.ainv_store.release();
-        } else {
-            as2.ainv_store.alloc(static_cast<size_t>(T) * rowsK * ldk);
-            CK(cudaMemsetAsync(as2.ainv_store.ptr, 0, as2.ainv_store.count * sizeof(double), stream));
-            as2.ainv32.release();
-        }
-        DevBuf<double> dAll, work;
-        DevBuf<int> infos;
-        dAll.upload(Aall.data(), Aall.size(), stream);
-        infos.alloc(static_cast<size_t>(2 * T + 2));
-        CK(cudaMemsetAsync(infos.ptr, 0, infos.count * sizeof(int), stream));
-        std::vector<const double *> tab(T);
-        for (int t = 0; t < T; ++t) {
-            double *dA = dAll.ptr + static_cast<size_t>(t) * n * n;
-            spd_inverse_inplace(h, dA, static_cast<int>(n), work, infos.ptr + 2 * t);
-            if (as2.tc) {
-                as_pack_inverse_tf32_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
-                    dA, static_cast<int>(n), static_cast<int>(nn), as2.KP,
-                    as2.ainv32.ptr + static_cast<size_t>(t) * as2.NP * as2.KP);
-                tab[t] = nullptr;
-                continue;
-            }
-            double *dst = as2.ainv_store.ptr + static_cast<size_t>(t) * rowsK * ldk;
-            as_pack_inverse_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
-                dA, static_cast<int>(n), static_cast<int>(nn), static_cast<int>(ldk), dst, as_round_bits());
-            tab[t] = dst;
-        }
-        CK(cudaGetLastError());
-        as2.ainv_tab.upload(tab.data(), tab.size(), stream);
-        tick("local inverses (device)");
-        // --- 3. type-ordered panel rows (types padded to the small-GEMM tile height)
-        const size_t BML = as2.tc ? static_cast<size_t>(kTcBM) : K1SmallCfg::BM;
-        const size_t lstride = as2.tc ? static_cast<size_t>(as2.LD) : ldk;
-        std::vector<int> rowL(B, -1), tiles;
-        size_t row = 0;
-        {
-            std::vector<std::vector<int>> members(T);
-            for (size_t cell = 0; cell < B; ++cell) members[type_of[cell]].push_back(static_cast<int>(cell));
-            for (int t = 0; t < T; ++t) {
-                const size_t first = row;
-                for (int cell : members[t]) rowL[cell] = static_cast<int>(row++);
-                row = first + round_up(row - first, BML);
-                for (size_t k = first / BML; k < row / BML; ++k) tiles.push_back(t);
-            }
-        }
-        as2.BL_pad = row;
-        as2.mtiles = row / BML;
-        if (as2.BL_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
-        as2.tile_type.upload(tiles.data(), tiles.size(), stream);
-        std::vector<int> s2(nodes * 4, -1);
-        for (size_t cell = 0; cell < B; ++cell) {
-            const uint32_t *dm = dofmap.data() + cell * n;
-            for (size_t rank = 0; rank < nn; ++rank) {
-                const size_t in = node_int_of_glob[dm[3 * rank] / 3];
-                int *sl = s2.data() + in * 4;
-                int k = 0;
-                while (sl[k] >= 0) ++k;
-                sl[k] = static_cast<int>(static_cast<size_t>(rowL[cell]) * lstride + rank);
-            }
-        }
-        as2.slots2.upload(s2.data(), s2.size(), stream);
-        if (as2.tc) {
-            if (as2.BL_pad * as2.LD >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
-            as2.XL32.alloc(as2.BL_pad * as2.LD);
-            CK(cudaMemsetAsync(as2.XL32.ptr, 0, as2.XL32.count * sizeof(float), stream));
-            as2.ZL32.alloc(as2.BL_pad * as2.LD);
-            as2.XL.release();
-            as2.ZL.release();
-            encode_tc_maps(T);
-        } else {
-            as2.XL.alloc(as2.BL_pad * ldk);
-            as2.ZL.alloc(as2.BL_pad * ldk);
-            CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
-            as2.XL32.release();
-            as2.ZL32.release();
-        }
-        as2.z.alloc(N);
-        tick("panel tables");
-        // --- 4. coarse space: corners of s x s super-blocks, bottom/top planes
+        DevBuf<double> work;
+        DevBuf<int> cinfo;
+        cinfo.alloc(2);
+        CK(cudaMemsetAsync(cinfo.ptr, 0, 2 * sizeof(int), stream));
+        // --- 1. coarse space (first: its dense inverse runs on the device while
+        // the host builds the local stage): corners of s x s super-blocks, bottom/top planes
         const uint32_t q = nl.n_x;
         const int sb = schwarz_super_block(rows, cols);
         if (node_super_ptr.size() != static_cast<size_t>(((cols + sb - 1) / sb) * ((rows + sb - 1) / sb)) + 1)
@@ -823,7 +668,7 @@ struct tsv_ctx {
             }
         const int nkeys = static_cast<int>(key_kind.size());
         tick("coarse keys");
-        if (dbg) std::fprintf(stderr, "[schwarz2] types %d keys %d s %d Nc %d n %zu\n", T, nkeys, sb, as2.Nc, n);
+        if (dbg) std::fprintf(stderr, "[schwarz2] keys %d s %d Nc %d n %zu\n", nkeys, sb, as2.Nc, n);
         std::vector<double> Kcall[2];
         {
             DevBuf<double> dP, dKP, dKc, dK;
@@ -873,7 +718,7 @@ struct tsv_ctx {
                         dk.ptr, as2.SX, as2.SY, px, py, as2.ainv_c.ptr, as2.Nc);
                 }
             as_fix_zero_rows_kernel<<<static_cast<unsigned>((Ncs + 7) / 8), 256, 0, stream>>>(as2.ainv_c.ptr, as2.Nc);
-            spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, infos.ptr + 2 * T);
+            spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, cinfo.ptr);
             as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
                                                                                                        as2.Nc);
             if (getenv_flag("TSV_AS_COARSE_F32")) {
@@ -886,12 +731,184 @@ struct tsv_ctx {
                 as2.ainv_c32.release();
             }
             CK(cudaGetLastError());
-            std::vector<int> hinfo(infos.count);
+        }
+        tick("coarse inverse (enqueued)");
+        // --- 2. neighbourhood types: own kind, the 4 edge neighbours' kinds
+        // (or absence), corner neighbours' presence, constrained pattern.
+        // Blocks of one type share the representative's local matrix
+        // (exact except for corner-neighbour kinds; TSV_AS_EXACT_TYPES=1
+        // makes corner kinds part of the type too).
+        tick("handles");
+        const bool exact_types = getenv_flag("TSV_AS_EXACT_TYPES");
+        std::map<std::vector<int>, int> sig_type;
+        std::vector<int> type_of(B), rep_of;
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t c = 0; c < cols; ++c) {
+                const size_t cell = static_cast<size_t>(r) * cols + c;
+                std::vector<int> sig;
+                sig.push_back(layout.kind_at(cell));
+                for (int dr = -1; dr <= 1; ++dr)
+                    for (int dc = -1; dc <= 1; ++dc) {
+                        if (!dr && !dc) continue;
+                        const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
+                        const bool in = rr >= 0 && cc >= 0 && rr < rows && cc < cols;
+                        const int kd = in ? layout.kind_at(static_cast<size_t>(rr) * cols + static_cast<size_t>(cc)) : -1;
+                        sig.push_back((dr && dc && !exact_types) ? (in ? 0 : -1) : kd);
+                    }
+                const uint32_t *dm = dofmap.data() + cell * n;
+                for (size_t a = 0; a < n; ++a)
+                    if (constrained[dm[a]]) sig.push_back(1000 + static_cast<int>(a));
+                auto it = sig_type.find(sig);
+                if (it == sig_type.end()) {
+                    it = sig_type.emplace(sig, static_cast<int>(rep_of.size())).first;
+                    rep_of.push_back(static_cast<int>(cell));
+                }
+                type_of[cell] = it->second;
+            }
+        const int T = static_cast<int>(rep_of.size());
+        as2.ntypes = T;
+        tick("types");
+        // --- 3. local matrices A_b = R_b A R_b^T (lifted), assembled on host
+        // threads, inverted in place on the device, packed by a kernel.
+        std::vector<double> Aall(static_cast<size_t>(T) * n * n, 0.0);
+        {
+            const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), static_cast<unsigned>(T)));
+            std::vector<std::thread> pool;
+            for (unsigned w = 0; w < nt; ++w)
+                pool.emplace_back([&, w] {
+                    std::vector<int> idx(n);
+                    for (int t = static_cast<int>(w); t < T; t += static_cast<int>(nt)) {
+                        double *A = Aall.data() + static_cast<size_t>(t) * n * n;  // column-major
+                        const size_t cell = static_cast<size_t>(rep_of[t]);
+                        const uint32_t r = static_cast<uint32_t>(cell / cols), c = static_cast<uint32_t>(cell % cols);
+                        const uint32_t *dm = dofmap.data() + cell * n;
+                        std::unordered_map<uint32_t, int> loc;
+                        loc.reserve(2 * n);
+                        for (size_t a = 0; a < n; ++a) loc[dm[a]] = static_cast<int>(a);
+                        for (int dr = -1; dr <= 1; ++dr)
+                            for (int dc = -1; dc <= 1; ++dc) {
+                                const long rr = static_cast<long>(r) + dr, cc = static_cast<long>(c) + dc;
+                                if (rr < 0 || cc < 0 || rr >= rows || cc >= cols) continue;
+                                const size_t b2 = static_cast<size_t>(rr) * cols + static_cast<size_t>(cc);
+                                const uint32_t *dm2 = dofmap.data() + b2 * n;
+                                const std::vector<double> &K2 = rom[layout.kind_at(b2)].k_r;
+                                for (size_t a = 0; a < n; ++a) {
+                                    auto f = loc.find(dm2[a]);
+                                    idx[a] = f == loc.end() ? -1 : f->second;
+                                }
+                                for (size_t a = 0; a < n; ++a) {
+                                    if (idx[a] < 0) continue;
+                                    for (size_t q2 = 0; q2 < n; ++q2)
+                                        if (idx[q2] >= 0) A[static_cast<size_t>(idx[q2]) * n + idx[a]] += K2[a * n + q2];
+                                }
+                            }
+                        for (size_t a = 0; a < n; ++a)
+                            if (constrained[dm[a]]) {
+                                for (size_t k = 0; k < n; ++k) A[a * n + k] = A[k * n + a] = 0.0;
+                                A[a * n + a] = 1.0;
+                            }
+                    }
+                });
+            for (auto &th : pool) th.join();
+        }
+        tick("local assembly (host)");
+        as2.tc = !getenv_flag("TSV_AS_LOCAL_F64") && as_round_bits() == 0;
+        const size_t rowsK = round_up(n, kBN);
+        if (as2.tc) {
+            as2.KP = static_cast<int>(round_up(n, kTcBK));
+            as2.ntn = static_cast<int>((n + 255) / 256);
+            as2.BN = static_cast<int>(round_up((n + as2.ntn - 1) / as2.ntn, 16));
+            as2.NP = as2.ntn * as2.BN;
+            as2.LD = std::max(as2.KP, as2.NP);
+            as2.ainv32.alloc(static_cast<size_t>(T) * as2.NP * as2.KP);
+            CK(cudaMemsetAsync(as2.ainv32.ptr, 0, as2.ainv32.count * sizeof(float), stream));
+            as2.ainv_store.release();
+        } else {
+            as2.ainv_store.alloc(static_cast<size_t>(T) * rowsK * ldk);
+            CK(cudaMemsetAsync(as2.ainv_store.ptr, 0, as2.ainv_store.count * sizeof(double), stream));
+            as2.ainv32.release();
+        }
+        DevBuf<double> dAll;
+        DevBuf<int> infos;
+        dAll.upload(Aall.data(), Aall.size(), stream);
+        infos.alloc(static_cast<size_t>(2 * T + 2));
+        CK(cudaMemsetAsync(infos.ptr, 0, infos.count * sizeof(int), stream));
+        std::vector<const double *> tab(T);
+        for (int t = 0; t < T; ++t) {
+            double *dA = dAll.ptr + static_cast<size_t>(t) * n * n;
+            spd_inverse_inplace(h, dA, static_cast<int>(n), work, infos.ptr + 2 * t);
+            if (as2.tc) {
+                as_pack_inverse_tf32_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
+                    dA, static_cast<int>(n), static_cast<int>(nn), as2.KP,
+                    as2.ainv32.ptr + static_cast<size_t>(t) * as2.NP * as2.KP);
+                tab[t] = nullptr;
+                continue;
+            }
+            double *dst = as2.ainv_store.ptr + static_cast<size_t>(t) * rowsK * ldk;
+            as_pack_inverse_kernel<<<static_cast<unsigned>((n * n + 255) / 256), 256, 0, stream>>>(
+                dA, static_cast<int>(n), static_cast<int>(nn), static_cast<int>(ldk), dst, as_round_bits());
+            tab[t] = dst;
+        }
+        CK(cudaGetLastError());
+        as2.ainv_tab.upload(tab.data(), tab.size(), stream);
+        tick("local inverses (device)");
+        // --- 4. type-ordered panel rows (types padded to the small-GEMM tile height)
+        const size_t BML = as2.tc ? static_cast<size_t>(kTcBM) : K1SmallCfg::BM;
+        const size_t lstride = as2.tc ? static_cast<size_t>(as2.LD) : ldk;
+        std::vector<int> rowL(B, -1), tiles;
+        size_t row = 0;
+        {
+            std::vector<std::vector<int>> members(T);
+            for (size_t cell = 0; cell < B; ++cell) members[type_of[cell]].push_back(static_cast<int>(cell));
+            for (int t = 0; t < T; ++t) {
+                const size_t first = row;
+                for (int cell : members[t]) rowL[cell] = static_cast<int>(row++);
+                row = first + round_up(row - first, BML);
+                for (size_t k = first / BML; k < row / BML; ++k) tiles.push_back(t);
+            }
+        }
+        as2.BL_pad = row;
+        as2.mtiles = row / BML;
+        if (as2.BL_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
+        as2.tile_type.upload(tiles.data(), tiles.size(), stream);
+        std::vector<int> s2(nodes * 4, -1);
+        for (size_t cell = 0; cell < B; ++cell) {
+            const uint32_t *dm = dofmap.data() + cell * n;
+            for (size_t rank = 0; rank < nn; ++rank) {
+                const size_t in = node_int_of_glob[dm[3 * rank] / 3];
+                int *sl = s2.data() + in * 4;
+                int k = 0;
+                while (sl[k] >= 0) ++k;
+                sl[k] = static_cast<int>(static_cast<size_t>(rowL[cell]) * lstride + rank);
+            }
+        }
+        as2.slots2.upload(s2.data(), s2.size(), stream);
+        if (as2.tc) {
+            if (as2.BL_pad * as2.LD >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
+            as2.XL32.alloc(as2.BL_pad * as2.LD);
+            CK(cudaMemsetAsync(as2.XL32.ptr, 0, as2.XL32.count * sizeof(float), stream));
+            as2.ZL32.alloc(as2.BL_pad * as2.LD);
+            as2.XL.release();
+            as2.ZL.release();
+            encode_tc_maps(T);
+        } else {
+            as2.XL.alloc(as2.BL_pad * ldk);
+            as2.ZL.alloc(as2.BL_pad * ldk);
+            CK(cudaMemsetAsync(as2.XL.ptr, 0, as2.XL.count * sizeof(double), stream));
+            as2.XL32.release();
+            as2.ZL32.release();
+        }
+        as2.z.alloc(N);
+        tick("panel tables");
+        {
+            std::vector<int> hinfo(infos.count), hc(2);
             d2h(hinfo.data(), infos.ptr, hinfo.size() * sizeof(int), stream);
+            d2h(hc.data(), cinfo.ptr, hc.size() * sizeof(int), stream);
+            hinfo.insert(hinfo.end(), hc.begin(), hc.end());
             for (int v : hinfo)
                 if (v != 0) throw StatusError(TSV_EINVAL, "schwarz2: local/coarse matrix not positive definite");
         }
-        tick("coarse inverse");
+        tick("done");
         as2.setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
 
@@ -1802,6 +1819,7 @@ int tsv_get_load(tsv_ctx *ctx, double *bout) {
         if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_load: no layout set");
         cudaSetDevice(ctx->device);
         std::vector<double> bi(ctx->N);
+        ctx->ensure_rhs();
         d2h(bi.data(), ctx->b.ptr, ctx->N * sizeof(double), ctx->stream);
         ctx->to_reference(bi.data(), bout);
         return TSV_OK;
@@ -1897,6 +1915,7 @@ int tsv_solve(tsv_ctx *ctx, const tsv_iter_options *opts, double *u_out, tsv_sol
     return guarded(ctx, [&] {
         if (!opts) throw StatusError(TSV_EINVAL, "solve: NULL options");
         cudaSetDevice(ctx->device);
+        ctx->ensure_rhs();
         return ctx->solve(*opts, u_out, info);
     });
 }
