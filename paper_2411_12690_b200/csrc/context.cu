@@ -721,7 +721,7 @@ struct tsv_ctx {
             spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, cinfo.ptr);
             as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
                                                                                                        as2.Nc);
-            if (getenv_flag("TSV_AS_COARSE_F32")) {
+            if (!getenv_flag("TSV_AS_COARSE_F64")) {
                 as2.ldc32 = static_cast<int>(round_up(Ncs, 32));
                 as2.ainv_c32.alloc(Ncs * as2.ldc32);
                 const size_t tot = Ncs * as2.ldc32;

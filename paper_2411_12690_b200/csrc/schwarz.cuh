@@ -37,9 +37,9 @@ struct AsParams {
     double *cellpart;      // [ncells][24]
     double *rc, *zc;       // coarse vectors [Nc]
     const double *ainv_c;  // dense [Nc][Nc]
-    const float *ainv_c32; // optional FP32 copy [Nc][ldc32] (TSV_AS_COARSE_F32: halves the coarse HBM
-                           // stream, but with the TF32 local solves it multiplies the residual-check
-                           // restarts near tol 1e-12 at config 3: 124-158 vs 79-84 iterations)
+    const float *ainv_c32; // FP32 copy [Nc][ldc32] (default; TSV_AS_COARSE_F64 keeps FP64): halves the
+                           // coarse HBM stream. With the FP64 DMMA true-residual check it raised the
+                           // restart count at tol 1e-12; with the exact int8 check it does not.
     int ldc32;
     int Nc;
     int round_bits;        // experiment: round the local-solve operand to this many mantissa bits (0 = off)
