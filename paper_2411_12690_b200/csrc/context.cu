@@ -196,6 +196,8 @@ struct tsv_ctx {
     DevBuf<double> sk_work;
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t side = nullptr;                       // Schwarz coarse chain (forked in the graph)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
 
     ~tsv_ctx() {
@@ -203,6 +205,9 @@ struct tsv_ctx {
         if (h_state) cudaFreeHost(h_state);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -1016,15 +1021,22 @@ struct tsv_ctx {
     void launch_as_update_precond(const CgParams &q) {
         AsParams a = as_params();
         as_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        // fork: the coarse chain (restrict -> coarse rhs -> coarse solve, HBM
+        // and latency bound) runs on a side stream beside the local solves
+        // (tensor cores); both join before z. Captured as a forked graph.
+        CK(cudaEventRecord(ev_fork, stream));
+        CK(cudaStreamWaitEvent(side, ev_fork, 0));
+        as_restrict_kernel<<<as2.ncells, 256, 0, side>>>(q, a);
+        as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, side>>>(q, a);
+        as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
+        CK(cudaEventRecord(ev_join, side));
         if (as2.tc) {
             launch_tc_local();
         } else {
             GemmParams gp = local_gemm_params();
             gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
         }
-        as_restrict_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
-        as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, stream>>>(q, a);
-        as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, stream>>>(q, a);
+        CK(cudaStreamWaitEvent(stream, ev_join, 0));
         as_z_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
         launches += 6;
     }
@@ -1587,6 +1599,9 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
     if (e != cudaSuccess) return TSV_ECUDA;
     int rc = guarded(ctx.get(), [&] {
         CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreate(&ctx->ev0));
         CK(cudaEventCreate(&ctx->ev1));
         CK(cudaMallocHost(&ctx->h_state, sizeof(CgState)));
