@@ -215,6 +215,12 @@ typedef struct {
 } tsv_rom_out;
 
 int tsv_rom_dims(const tsv_local_desc *desc, uint64_t *n, uint64_t *n_fine, uint64_t *cells);
+/* rom_fingerprint (rom.cpp:110-132) of a configuration (host only), and the
+ * kind + stored fingerprint of a .rom file (header checked like load_rom):
+ * what cmd_solve's "ROM ... was built for a different configuration" check
+ * (cli.cpp:38-44) compares. */
+int tsv_rom_fingerprint(const tsv_local_desc *desc, uint8_t fingerprint[32]);
+int tsv_rom_file_info(const char *path, int *kind, uint8_t fingerprint[32], char *err, size_t err_len);
 int tsv_build_rom(int device, const tsv_local_desc *desc, tsv_rom_out *out, char *err, size_t err_len);
 
 /* Page-lock a host buffer so tsv_recover / tsv_solve copies run at full

@@ -464,4 +464,30 @@ int ref_stress_grid_save_csv(const double *values, uint32_t rows, uint32_t cols,
     });
 }
 
+// default_grading (mesh.cpp:106-119) and rom_fingerprint (rom.cpp:110-132)
+// of a geometry with the default materials and a q^3 node layout: pins the
+// product CLI's restatement (tests/test_cli.py). Axis lengths in len[3];
+// x/y/z must hold cap values each.
+int ref_default_grading(double d, double h, double t, double p, double target, uint32_t q, uint32_t cap, double* x,
+                        double* y, double* z, uint32_t* len, uint8_t* fingerprint) {
+    return guarded([&] {
+        UnitBlockGeometry geom;
+        geom.d = d;
+        geom.h = h;
+        geom.t = t;
+        geom.p = p;
+        TensorGrid g = default_grading(geom, target);
+        const std::vector<double>* axes[3] = {&g.x, &g.y, &g.z};
+        double* outs[3] = {x, y, z};
+        for (int a = 0; a < 3; ++a) {
+            if (axes[a]->size() > cap) throw Error("ref_default_grading: axis longer than cap");
+            len[a] = static_cast<uint32_t>(axes[a]->size());
+            std::memcpy(outs[a], axes[a]->data(), axes[a]->size() * sizeof(double));
+        }
+        rom::NodeLayout nl = rom::NodeLayout::create(q, q, q, p, p, h);
+        Hash256 fp = rom::rom_fingerprint(geom, g, MaterialTable::defaults(), nl);
+        std::memcpy(fingerprint, fp.data(), 32);
+    });
+}
+
 }  // extern "C"

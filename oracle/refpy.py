@@ -256,3 +256,16 @@ def stress_grid_save_csv(values, rows, cols, res, pitch, path):
     v = np.ascontiguousarray(values, np.float64)
     if L.ref_stress_grid_save_csv(_ptr(v), rows, cols, res, pitch, path.encode()) != 0:
         raise RefError(_err())
+
+
+def default_grading(d, h, t, p, target, q=4):
+    """The reference's default_grading + rom_fingerprint (default materials)."""
+    L = lib()
+    L.ref_default_grading.argtypes = [C.c_double] * 5 + [C.c_uint32, C.c_uint32] + [C.c_void_p] * 5
+    cap = 4096
+    axes = [np.empty(cap) for _ in range(3)]
+    ln = np.zeros(3, np.uint32)
+    fp = np.zeros(32, np.uint8)
+    if L.ref_default_grading(d, h, t, p, target, q, cap, *(_ptr(a) for a in axes), _ptr(ln), _ptr(fp)) != 0:
+        raise RefError(_err())
+    return [axes[a][:ln[a]].copy() for a in range(3)], bytes(fp)

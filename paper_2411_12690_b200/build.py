@@ -15,6 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libtsv_b200.so")
+CLI = os.path.join(OUT_DIR, "tsvstress_b200")  # `local` / `solve` commands over the C ABI
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -23,6 +24,7 @@ NVCC_FLAGS = [
     "--expt-relaxed-constexpr",
 ]
 SOURCES = ["context.cu", "local_stage.cu", "host_index.cpp", "rom_io.cpp"]
+CLI_SOURCE = "cli_main.cpp"
 LIBS = ["-lcusolver", "-lcublas", "-lcrypto", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
 
 
@@ -34,7 +36,7 @@ def _nvcc():
 
 
 def _stale():
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(CLI):
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "tsv_b200.h")]
@@ -62,6 +64,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(CSRC, CLI_SOURCE), "-o", CLI + ".tmp",
+           "-L", OUT_DIR, "-ltsv_b200", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(CLI + ".tmp", CLI)
     return LIB
 
 

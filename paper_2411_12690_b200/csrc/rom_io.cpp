@@ -133,6 +133,23 @@ void put(std::string &s, T v) {
     s.append(reinterpret_cast<const char *>(&v), sizeof(T));
 }
 
+// rom_fingerprint's byte stream (rom.cpp:110-132), also the .rom header.
+std::string header_bytes(const double geometry[4], const uint32_t grid_len[3], const double *const grid[3],
+                         const double materials[3][3], const uint32_t q[3]) {
+    std::string header;
+    for (int i = 0; i < 4; ++i) put(header, geometry[i]);
+    for (int a = 0; a < 3; ++a) {
+        put(header, grid_len[a]);
+        header.append(reinterpret_cast<const char *>(grid[a]), grid_len[a] * sizeof(double));
+    }
+    for (uint8_t id = 0; id < 3; ++id) {
+        put(header, id);
+        for (int k = 0; k < 3; ++k) put(header, materials[id][k]);
+    }
+    for (int a = 0; a < 3; ++a) put(header, q[a]);
+    return header;
+}
+
 }  // namespace
 
 extern "C" {
@@ -151,20 +168,32 @@ int tsv_load_rom_file(tsv_ctx *ctx, int slot, const char *path, int *kind_out, c
     }
 }
 
+int tsv_rom_fingerprint(const tsv_local_desc *d, uint8_t out[32]) {
+    if (!d || !out) return TSV_EINVAL;
+    for (int a = 0; a < 3; ++a)
+        if (!d->grid[a] || d->grid_len[a] < 2) return TSV_EINVAL;
+    const std::string h = header_bytes(d->geometry, d->grid_len, d->grid, d->materials, d->q);
+    SHA256(reinterpret_cast<const unsigned char *>(h.data()), h.size(), out);
+    return TSV_OK;
+}
+
+int tsv_rom_file_info(const char *path, int *kind_out, uint8_t fingerprint[32], char *err, size_t err_len) {
+    try {
+        LoadedRom m = parse(path ? path : "");
+        if (kind_out) *kind_out = m.kind;
+        if (fingerprint) std::memcpy(fingerprint, m.desc.fingerprint, 32);
+        if (err && err_len) err[0] = 0;
+        return TSV_OK;
+    } catch (const std::exception &e) {
+        if (err && err_len) std::snprintf(err, err_len, "%s", e.what());
+        return TSV_EINVAL;
+    }
+}
+
 int tsv_save_rom_file(const tsv_rom_desc *d, int kind, const char *path, char *err, size_t err_len) {
     try {
         if (!d || !path) throw IoError("save_rom: NULL argument");
-        std::string header;
-        for (int i = 0; i < 4; ++i) put(header, d->geometry[i]);
-        for (int a = 0; a < 3; ++a) {
-            put(header, d->grid_len[a]);
-            header.append(reinterpret_cast<const char *>(d->grid[a]), d->grid_len[a] * sizeof(double));
-        }
-        for (uint8_t id = 0; id < 3; ++id) {
-            put(header, id);
-            for (int k = 0; k < 3; ++k) put(header, d->materials[id][k]);
-        }
-        for (int a = 0; a < 3; ++a) put(header, d->q[a]);
+        const std::string header = header_bytes(d->geometry, d->grid_len, d->grid, d->materials, d->q);
         unsigned char fp[32];
         SHA256(reinterpret_cast<const unsigned char *>(header.data()), header.size(), fp);
         const size_t nf = 3ull * d->grid_len[0] * d->grid_len[1] * d->grid_len[2];

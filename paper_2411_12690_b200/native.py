@@ -19,7 +19,7 @@ EXPORTS = [
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
     "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_precond_apply", "tsv_precond_setup", "tsv_debug_coarse", "tsv_solve", "tsv_set_solution", "tsv_recover",
     "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
-    "tsv_rom_dims", "tsv_build_rom", "tsv_load_rom_file", "tsv_save_rom_file", "tsv_host_register", "tsv_host_unregister", "tsv_fp64_peak",
+    "tsv_rom_dims", "tsv_rom_fingerprint", "tsv_rom_file_info", "tsv_build_rom", "tsv_load_rom_file", "tsv_save_rom_file", "tsv_host_register", "tsv_host_unregister", "tsv_fp64_peak",
 ]
 
 
@@ -118,6 +118,8 @@ def load(path: str = LIB_PATH):
         "tsv_fp64_peak": (i, [i, P(d), P(d)]),
         "tsv_load_rom_file": (i, [vp, i, C.c_char_p, P(i), C.c_char_p, sz]),
         "tsv_save_rom_file": (i, [P(RomDesc), i, C.c_char_p, C.c_char_p, sz]),
+        "tsv_rom_fingerprint": (i, [P(LocalDesc), vp]),
+        "tsv_rom_file_info": (i, [C.c_char_p, P(i), vp, C.c_char_p, sz]),
         "tsv_rom_dims": (i, [P(LocalDesc), P(u64), P(u64), P(u64)]),
         "tsv_build_rom": (i, [i, P(LocalDesc), P(RomOut), C.c_char_p, sz]),
     }
