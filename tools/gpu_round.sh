@@ -1,0 +1,14 @@
+#!/bin/bash
+# One GPU-box pass: tests, smoke, bench (both arms), launch list of the bench command.
+# Usage: tools/gpu_round.sh [tag]   (outputs under gpurun_out/<tag>/)
+tag=${1:-r1}
+out=gpurun_out/$tag
+mkdir -p $out
+nvidia-smi > $out/nvidia-smi.txt 2>&1
+timeout 2400 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 2>&1; echo "smoke exit $?" >> $out/smoke.log
+timeout 900 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench exit $?" >> $out/bench.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_ref.json 2> $out/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-jacobi-leg --no-cpu-baseline --e2e-steps 1 > $out/ncu_bench.log 2>&1
+echo "ncu exit $?" >> $out/ncu_bench.log
