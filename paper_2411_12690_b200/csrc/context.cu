@@ -1423,10 +1423,11 @@ struct tsv_ctx {
         sp.out = out;
         sp.out_cell0 = static_cast<long long>(c0);
         sp.out_cells = static_cast<long long>(c1 - c0);
-        const size_t smem = (((2 * (m.cells[0] + 1) * (m.cells[1] + 1) * 3 + 1) & ~size_t(1)) + kStressThreads * 7) * sizeof(double);
-        if (points > 0 && smem > 48 * 1024) {
+        const size_t smem = stress_smem_bytes(points > 0 ? points : 1, static_cast<int>(m.cells[0]), static_cast<int>(m.cells[1]));
+        if (points > 0) {
             if (smem > 227 * 1024) throw StatusError(TSV_EINVAL, "recover: element layer too large for shared memory");
-            CK(cudaFuncSetAttribute(stress_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            if (points == 8) CK(cudaFuncSetAttribute(stress_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            else CK(cudaFuncSetAttribute(stress_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         }
         size_t t = 0;
         while (t < m_tiles) {
@@ -1452,12 +1453,14 @@ struct tsv_ctx {
             gp.col_bias[0] = gp.col_bias[1] = mk.d_ut.ptr;
             gp.done = nullptr;
             gp.tile_counter = tile_counter.ptr;
+            gp.n_major = 1;
             gemm_nt_f64<K6Cfg><<<k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
             if (points > 0) {
                 sp.U = U.ptr;
                 sp.j0 = static_cast<int>(t * kBM);
-                dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>(m.cells[2]));
-                stress_kernel<<<grid, kStressThreads, smem, stream>>>(sp);
+                dim3 grid(static_cast<unsigned>(m.cells[2]), static_cast<unsigned>((t1 - t) * kBM));
+                if (points == 8) stress_kernel<8><<<grid, kStressThreads, smem, stream>>>(sp);
+                else stress_kernel<1><<<grid, kStressThreads, smem, stream>>>(sp);
             } else {
                 const int res = -points;
                 CutParams cp{};

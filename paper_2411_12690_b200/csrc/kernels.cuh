@@ -39,6 +39,8 @@ struct GemmParams {
     const int *done;             // nullable: early exit when *done != 0
     const int *skip_flag;        // nullable: early exit when *skip_flag != 0 (hybrid K1: A x goes to int8)
     unsigned *tile_counter;      // [2] {next tile, exited CTAs}, zero between launches
+    int n_major;                 // tile order: 0 = M major (K1: A streamed once, K_r in L2),
+                                 // 1 = N major (K6: Phi streamed once, the Q chunk in L2)
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -222,7 +224,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
         const int tile = s_tile;
         __syncthreads();
         if (tile >= total) break;
-        const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        const int mt = p.n_major ? tile % p.m_tiles : tile / p.n_tiles;
+        const int nt = p.n_major ? tile / p.m_tiles : tile % p.n_tiles;
         double acc[Cfg::FM][Cfg::FN][2];
 #pragma unroll
         for (int i = 0; i < Cfg::FM; ++i)
@@ -676,101 +679,146 @@ struct StressParams {
     long long out_cells;      // cells in the output range
 };
 
-// One CTA per (block, element layer). The two node layers of u are staged
-// in shared memory; points are processed in tiles of blockDim.x (one per
-// thread); each tile's 7-value records are staged in shared memory and
-// written out as contiguous 16-byte streaming stores (the layer's output is
-// one contiguous range of out).
-constexpr int kStressThreads = 256;
+// One CTA per (element layer, block): the two node layers of u are staged in
+// shared memory, one thread evaluates one element at all its P points. The
+// gradients of a trilinear box element are separable: du_c/dx depends on
+// (eta, zeta) only, du_c/dy on (xi, zeta), du_c/dz on (xi, eta), so the 9
+// derivatives take 4 distinct values each over the 8 Gauss points; they are
+// formed once per element from the 12 edge differences (fem.cpp:27-58 with a
+// diagonal Jacobian) and reused, leaving ~40 FP64 operations per point.
+// Output: each warp stages one xi-half of its 32 elements' records (4 points
+// x 7 values = 224 B = 7 whole sectors per element) in shared memory with an
+// odd per-element stride (conflict-free) and streams them out, so the staging
+// area stays small enough for 4 CTAs per SM.
+constexpr int kStressThreads = 128;
+constexpr int kStressWarps = kStressThreads / 32;
 
-__global__ void __launch_bounds__(kStressThreads) stress_kernel(StressParams sp) {
-    extern __shared__ double su[];  // two node layers: 2 * nxy * 3, then the output tile
-    const int jr = blockIdx.x;       // row within chunk
-    const int k = blockIdx.y;        // element layer
+__host__ __device__ constexpr int stress_halves(int P) { return P == 8 ? 2 : 1; }
+__host__ __device__ constexpr int stress_stride(int P) { return (P / stress_halves(P) * 7) | 1; }
+inline size_t stress_smem_bytes(int P, int cx, int cy) {
+    return (static_cast<size_t>(kStressWarps) * 32 * stress_stride(P) + 9 + cx + cy +
+            2 * static_cast<size_t>(cx + 1) * (cy + 1) * 3) * sizeof(double);
+}
+
+// Bilinear form over two natural coordinates s1, s2 in {-g, +g} of the edge
+// differences D[a][b] (a along s1, b along s2), scaled by q:
+//   out[(s1 > 0) << 1 | (s2 > 0)] = q sum_ab w_a(s1) w_b(s2) D[a][b],  w_0 = 1 - s, w_1 = 1 + s.
+__device__ __forceinline__ void stress_bilinear(double d00, double d10, double d01, double d11, double q,
+                                                double out[4]) {
+    constexpr double g = 0.57735026918962576451;  // 1/sqrt(3)
+    const double A = 1.0 + g, Bm = 1.0 - g;
+    const double t0m = fma(A, d00, Bm * d10), t1m = fma(A, d01, Bm * d11);  // s1 = -g
+    const double t0p = fma(Bm, d00, A * d10), t1p = fma(Bm, d01, A * d11);  // s1 = +g
+    const double qA = q * A, qB = q * Bm;
+    out[0] = fma(qA, t0m, qB * t1m);
+    out[1] = fma(qB, t0m, qA * t1m);
+    out[2] = fma(qA, t0p, qB * t1p);
+    out[3] = fma(qB, t0p, qA * t1p);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kStressThreads, 4) stress_kernel(StressParams sp) {
+    static_assert(P == 8 || P == 1, "Gauss 2x2x2 or centroid");
+    constexpr int REC = P * 7, HALVES = stress_halves(P), GPH = P / HALVES, RECH = GPH * 7;
+    constexpr int STR = stress_stride(P), NV = P == 8 ? 4 : 1;
+    extern __shared__ double sm[];
+    const int k = blockIdx.x;   // element layer
+    const int jr = blockIdx.y;  // row within chunk
     const int j = sp.j0 + jr;
     const int cell = sp.row_cell[j];
     if (cell < 0) return;
     const long long oc = cell - sp.out_cell0;
     if (oc < 0 || oc >= sp.out_cells) return;
     const int kind = sp.row_kind[j];
-    const int nx = sp.cx + 1, ny = sp.cy + 1, nxy = nx * ny;
+    const int cx = sp.cx, cy = sp.cy, nx = cx + 1, nxy = nx * (cy + 1);
+    double *stg = sm;                                  // [warp][32][STR]
+    double *ls = stg + kStressWarps * 32 * STR;        // lambda, mu, alpha(3 lambda + 2 mu) per material
+    double *hs = ls + 9;                               // 1/h along x (cx), then y (cy)
+    double *su = hs + cx + cy;                         // node layers k, k+1: [2][nxy][3]
     const double *U = sp.U + static_cast<long long>(jr) * sp.ldu + static_cast<long long>(k) * nxy * 3;
-    for (int i = threadIdx.x; i < 2 * nxy * 3; i += blockDim.x) su[i] = U[i];
-    double *tile = su + ((2 * nxy * 3 + 1) & ~1);  // 16-byte aligned
+    for (int i = threadIdx.x; i < 2 * nxy * 3; i += kStressThreads) su[i] = __ldg(U + i);
+    const double *hk = sp.hinv[kind];
+    for (int i = threadIdx.x; i < cx + cy; i += kStressThreads) hs[i] = hk[i];
+    if (threadIdx.x < 9) ls[threadIdx.x] = sp.lame[kind][threadIdx.x / 3][threadIdx.x % 3];
     __syncthreads();
     const double dt = sp.row_dt[j];
-    const double *hx = sp.hinv[kind], *hy = hx + sp.cx, *hz = hy + sp.cy;
-    const double hzi = hz[k];
-    const int P = sp.P;
-    const int per_layer = sp.cx * sp.cy * P;
-    const long long E = static_cast<long long>(sp.cx) * sp.cy * sp.cz;
-    const double g = 0.57735026918962576451;  // 1/sqrt(3)
-    double *out_layer = sp.out + (oc * E + static_cast<long long>(k) * sp.cx * sp.cy) * P * 7;
-    for (int t0 = 0; t0 < per_layer; t0 += blockDim.x) {
-        const int t = t0 + threadIdx.x;
-        if (t < per_layer) {
-            const int gp = t % P, e2 = t / P;
-            const int i = e2 % sp.cx, jj = e2 / sp.cx;
-            const long long e = (static_cast<long long>(k) * sp.cy + jj) * sp.cx + i;
-            double xi = 0.0, eta = 0.0, zeta = 0.0;
-            if (P == 8) {
-                xi = (gp >> 2) ? g : -g;
-                eta = ((gp >> 1) & 1) ? g : -g;
-                zeta = (gp & 1) ? g : -g;
-            }
-            const double hxi = hx[i], hyi = hy[jj];
-            // grad N_a = J^-1 dN/dxi with J = diag(h/2) for box cells (fem.cpp:27-58), summed
-            // separably: d/dx = hx/4 sum_{dj,dk} (1 +- eta)(1 +- zeta) (u[1,dj,dk] - u[0,dj,dk]), etc.
-            const double ex0 = 1.0 - xi, ex1 = 1.0 + xi, ey0 = 1.0 - eta, ey1 = 1.0 + eta;
-            const double ez0 = 1.0 - zeta, ez1 = 1.0 + zeta;
-            const double qx = 0.25 * hxi, qy = 0.25 * hyi, qz = 0.25 * hzi;
-            const double *u000 = su + (jj * nx + i) * 3, *u100 = u000 + 3, *u010 = u000 + nx * 3, *u110 = u010 + 3;
-            const double *u001 = u000 + nxy * 3, *u101 = u001 + 3, *u011 = u001 + nx * 3, *u111 = u011 + 3;
-            double du[3][3];
+    const double qz = 0.25 * hk[cx + cy + k];
+    const int ne = cx * cy;
+    const long long E = static_cast<long long>(cx) * cy * sp.cz;
+    double *out_layer = sp.out + (oc * E + static_cast<long long>(k) * ne) * REC;
+    const uint8_t *emat = sp.elem_mat[kind] + static_cast<long long>(k) * ne;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *wst = stg + warp * 32 * STR;
+    for (int base = warp * 32; base < ne; base += kStressThreads) {
+        const int e2 = base + lane;
+        const bool live = e2 < ne;
+        double dux[3][NV], duy[3][NV], duz[3][NV];
+        double lambda = 0.0, mu = 0.0, thermal = 0.0;
+        if (live) {
+            const int i = e2 % cx, jj = e2 / cx;
+            const double qx = 0.25 * hs[i], qy = 0.25 * hs[cx + jj];
+            const double *u0 = su + (jj * nx + i) * 3;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const double v000 = u000[c], v100 = u100[c], v010 = u010[c], v110 = u110[c];
-                const double v001 = u001[c], v101 = u101[c], v011 = u011[c], v111 = u111[c];
-                du[c][0] = qx * (ez0 * (ey0 * (v100 - v000) + ey1 * (v110 - v010)) +
-                                 ez1 * (ey0 * (v101 - v001) + ey1 * (v111 - v011)));
-                du[c][1] = qy * (ez0 * (ex0 * (v010 - v000) + ex1 * (v110 - v100)) +
-                                 ez1 * (ex0 * (v011 - v001) + ex1 * (v111 - v101)));
-                du[c][2] = qz * (ey0 * (ex0 * (v001 - v000) + ex1 * (v101 - v100)) +
-                                 ey1 * (ex0 * (v011 - v010) + ex1 * (v111 - v110)));
+                const double v000 = u0[c], v100 = u0[3 + c], v010 = u0[nx * 3 + c], v110 = u0[nx * 3 + 3 + c];
+                const double v001 = u0[nxy * 3 + c], v101 = u0[nxy * 3 + 3 + c];
+                const double v011 = u0[(nxy + nx) * 3 + c], v111 = u0[(nxy + nx) * 3 + 3 + c];
+                // edge differences: x-edges at (y, z), y-edges at (x, z), z-edges at (x, y)
+                const double x00 = v100 - v000, x10 = v110 - v010, x01 = v101 - v001, x11 = v111 - v011;
+                const double y00 = v010 - v000, y10 = v110 - v100, y01 = v011 - v001, y11 = v111 - v101;
+                const double z00 = v001 - v000, z10 = v101 - v100, z01 = v011 - v010, z11 = v111 - v110;
+                if constexpr (P == 8) {
+                    stress_bilinear(x00, x10, x01, x11, qx, dux[c]);  // (eta, zeta)
+                    stress_bilinear(y00, y10, y01, y11, qy, duy[c]);  // (xi, zeta)
+                    stress_bilinear(z00, z10, z01, z11, qz, duz[c]);  // (xi, eta)
+                } else {
+                    dux[c][0] = qx * ((x00 + x10) + (x01 + x11));
+                    duy[c][0] = qy * ((y00 + y10) + (y01 + y11));
+                    duz[c][0] = qz * ((z00 + z10) + (z01 + z11));
+                }
             }
-            const int mat = sp.elem_mat[kind][e];
-            const double lambda = sp.lame[kind][mat][0], mu = sp.lame[kind][mat][1];
-            const double thermal = sp.lame[kind][mat][2] * dt;
-            const double exx = du[0][0], eyy = du[1][1], ezz = du[2][2];
-            const double exy = 0.5 * (du[0][1] + du[1][0]);
-            const double eyz = 0.5 * (du[1][2] + du[2][1]);
-            const double ezx = 0.5 * (du[2][0] + du[0][2]);
-            const double tr = exx + eyy + ezz;
-            const double sxx = lambda * tr + 2.0 * mu * exx - thermal;
-            const double syy = lambda * tr + 2.0 * mu * eyy - thermal;
-            const double szz = lambda * tr + 2.0 * mu * ezz - thermal;
-            const double sxy = 2.0 * mu * exy, syz = 2.0 * mu * eyz, szx = 2.0 * mu * ezx;
-            const double d1 = sxx - syy, d2 = syy - szz, d3 = szz - sxx;
-            const double vm2 = 0.5 * (d1 * d1 + d2 * d2 + d3 * d3) + 3.0 * (sxy * sxy + syz * syz + szx * szx);
-            double *o = tile + threadIdx.x * 7;
-            o[0] = sxx; o[1] = syy; o[2] = szz; o[3] = sxy; o[4] = syz; o[5] = szx;
-            o[6] = sqrt(fmax(vm2, 0.0));
+            const int mat = emat[e2];
+            lambda = ls[mat * 3];
+            mu = ls[mat * 3 + 1];
+            thermal = ls[mat * 3 + 2] * dt;
         }
-        __syncthreads();
-        // the tile's records are out_layer[t0*7 .. (t0+cnt)*7): contiguous
-        const int cnt = min(static_cast<int>(blockDim.x), per_layer - t0);
-        double *dst = out_layer + static_cast<long long>(t0) * 7;
-        const int nd = cnt * 7;
-        if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-            const int n2 = nd >> 1;
-            const double2 *src2 = reinterpret_cast<const double2 *>(tile);
-            double2 *dst2 = reinterpret_cast<double2 *>(dst);
-            for (int q = threadIdx.x; q < n2; q += blockDim.x) __stcs(dst2 + q, src2[q]);
-            if ((nd & 1) && threadIdx.x == 0) __stcs(dst + nd - 1, tile[nd - 1]);
-        } else {
-            for (int q = threadIdx.x; q < nd; q += blockDim.x) __stcs(dst + q, tile[q]);
+        const double mu2 = 2.0 * mu;
+        const int nel = min(32, ne - base);
+        double *dst = out_layer + static_cast<long long>(base) * REC;
+#pragma unroll
+        for (int h = 0; h < HALVES; ++h) {
+            if (live) {
+                double *o = wst + lane * STR;
+#pragma unroll
+                for (int gl = 0; gl < GPH; ++gl) {
+                    // gp = (xi bit) << 2 | (eta bit) << 1 | (zeta bit), zeta fastest (fem.cpp:87-92)
+                    const int gp = h * GPH + gl;
+                    const int ix = P == 8 ? (gp & 3) : 0;                        // (eta, zeta)
+                    const int iy = P == 8 ? (((gp >> 2) << 1) | (gp & 1)) : 0;  // (xi, zeta)
+                    const int iz = P == 8 ? (gp >> 1) : 0;                       // (xi, eta)
+                    const double exx = dux[0][ix], eyy = duy[1][iy], ezz = duz[2][iz];
+                    const double s0 = fma(lambda, exx + eyy + ezz, -thermal);
+                    const double sxx = fma(mu2, exx, s0), syy = fma(mu2, eyy, s0), szz = fma(mu2, ezz, s0);
+                    const double sxy = mu * (duy[0][iy] + dux[1][ix]);
+                    const double syz = mu * (duz[1][iz] + duy[2][iy]);
+                    const double szx = mu * (dux[2][ix] + duz[0][iz]);
+                    const double d1 = sxx - syy, d2 = syy - szz, d3 = szz - sxx;
+                    const double nrm = fma(d1, d1, fma(d2, d2, d3 * d3));
+                    const double shr = fma(sxy, sxy, fma(syz, syz, szx * szx));
+                    const double vm2 = fma(0.5, nrm, 3.0 * shr);
+                    o[gl * 7 + 0] = sxx; o[gl * 7 + 1] = syy; o[gl * 7 + 2] = szz;
+                    o[gl * 7 + 3] = sxy; o[gl * 7 + 4] = syz; o[gl * 7 + 5] = szx;
+                    o[gl * 7 + 6] = sqrt(fmax(vm2, 0.0));
+                }
+            }
+            __syncwarp();
+            // element el's half-record: dst[el*REC + h*RECH .. + RECH) (whole sectors when P = 8)
+            for (int q = lane; q < nel * RECH; q += 32) {
+                const int el = q / RECH, off = q - el * RECH;
+                __stcs(dst + el * REC + h * RECH + off, wst[el * STR + off]);
+            }
+            __syncwarp();
         }
-        __syncthreads();
     }
 }
 

@@ -10,5 +10,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.log 
 timeout 900 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench exit $?" >> $out/bench.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $out/bench_ref.json 2> $out/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-jacobi-leg --no-cpu-baseline --e2e-steps 1 > $out/ncu_bench.log 2>&1
+  python bench.py --steps 2 --warmup 3 --no-jacobi-leg --no-cpu-baseline --e2e-steps 0 > $out/ncu_bench.log 2>&1
 echo "ncu exit $?" >> $out/ncu_bench.log

@@ -11,6 +11,7 @@ g.set_roms(synth_rom(cfg, 0), synth_rom(cfg, 1) if cfg.dummy_seed else None)
 g.set_layout(ArrayLayout(cfg.rows, cfg.cols, cfg.kinds(), cfg.delta_t(), cfg.p, cfg.h))
 g.set_bc("bottom_pin_321")
 g.set_solution(np.random.default_rng(0).standard_normal(g.index().dof_count) * 1e-7)
-g.recover_resident(cfg.points)
-print("recover_ms", g.timing().recover_ms)
+for _ in range(int(os.environ.get("REPS", "1"))):
+    g.recover_resident(cfg.points)
+    print("recover_ms", g.timing().recover_ms, flush=True)
 g.close()
