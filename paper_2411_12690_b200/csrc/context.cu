@@ -62,16 +62,26 @@ struct StatusError : std::runtime_error {
                               std::string(#expr) + ": " + cudaGetErrorString(e_));                 \
     } while (0)
 
+// Stream-ordered device buffers: inside an ABI call (guarded()) allocations
+// and frees are queued on the context stream (cudaMallocAsync / cudaFreeAsync
+// from the device pool), so dropping a temporary never stalls the host on
+// the device (a plain cudaFree synchronises the whole device).
+thread_local cudaStream_t tl_alloc_stream = nullptr;
+
 template <typename T>
 struct DevBuf {
     T *ptr = nullptr;
     size_t count = 0;
+    cudaStream_t s_ = nullptr;  // stream the memory is ordered on (null: synchronous)
     DevBuf() = default;
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (ptr) cudaFree(ptr);
+        if (ptr) {
+            if (s_) cudaFreeAsync(ptr, s_);
+            else cudaFree(ptr);
+        }
         ptr = nullptr;
         count = 0;
     }
@@ -79,12 +89,39 @@ struct DevBuf {
         if (n == count && ptr) return;
         release();
         if (n == 0) return;
-        CK(cudaMalloc(&ptr, n * sizeof(T)));
+        s_ = tl_alloc_stream;
+        if (s_) CK(cudaMallocAsync(reinterpret_cast<void **>(&ptr), n * sizeof(T), s_));
+        else CK(cudaMalloc(&ptr, n * sizeof(T)));
         count = n;
     }
     void upload(const T *src, size_t n, cudaStream_t s) {
         alloc(n);
         if (n) CK(cudaMemcpyAsync(ptr, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+// TSV_TIMING=1: host wall time of the set-up phases on stderr (no syncs added).
+struct PhaseTimer {
+    const char *name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit PhaseTimer(const char *n) : name(n) {}
+    ~PhaseTimer() {
+        static const bool on = [] { const char *v = std::getenv("TSV_TIMING"); return v && *v && *v != '0'; }();
+        if (on)
+            std::fprintf(stderr, "[tsv timing] %-22s %8.2f ms\n", name,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
+// Owns a stream; declared first in tsv_ctx so it is destroyed after every
+// DevBuf member has queued its free on it.
+struct StreamOwner {
+    cudaStream_t s = nullptr;
+    ~StreamOwner() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
     }
 };
 
@@ -112,7 +149,7 @@ struct RomHost {
     std::vector<double> k_r, b_el, u_t;  // host copies used for assembly of b / preconditioners
     size_t n = 0, n_fine = 0, cells[3] = {0, 0, 0};
     uint8_t fingerprint[32] = {};
-    DevBuf<double> d_k, d_phi, d_ut, d_hinv, d_grid[3];
+    DevBuf<double> d_k, d_phi, d_ut, d_hinv, d_grid[3], d_bel;
     DevBuf<uint8_t> d_em;
     // Ozaki digit planes of K_r (int8 K1): [S][rows][KA], row exponents
     int oz_s = 0;
@@ -123,6 +160,7 @@ struct RomHost {
 }  // namespace
 
 struct tsv_ctx {
+    StreamOwner own_stream, own_side, own_copy;  // first: destroyed last
     int device = 0;
     cudaStream_t stream = nullptr;
     std::string err;
@@ -154,6 +192,8 @@ struct tsv_ctx {
     // device
     DevBuf<double> X, Y, b, x, r, p, ap, pre, partial, row_dt_d, U, stress;
     DevBuf<int> slots, row_cell_d;
+    DevBuf<uint32_t> glob_of_int_d;  // internal node -> reference node
+    DevBuf<double> uref;             // reference-ordered staging for D2H
     DevBuf<uint8_t> cmask, row_kind_d, tile_kind_d, tile_kind_small_d;
     DevBuf<unsigned> tile_counter;
     DevBuf<CgState> state;
@@ -197,6 +237,9 @@ struct tsv_ctx {
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaStream_t side = nullptr;                       // Schwarz coarse chain (forked in the graph)
+    cudaStream_t copy = nullptr;                       // recovery D2H (overlaps the next chunk)
+    cudaEvent_t rec_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // [computed, copied] x 2 staging buffers
+    DevBuf<double> rstage[2];
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
 
@@ -207,8 +250,12 @@ struct tsv_ctx {
         if (ev1) cudaEventDestroy(ev1);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
-        if (side) cudaStreamDestroy(side);
-        if (stream) cudaStreamDestroy(stream);
+        if (stream) cudaStreamSynchronize(stream);
+        if (copy) cudaStreamSynchronize(copy);
+        tl_alloc_stream = nullptr;
+        for (auto &e : rec_ev)
+            if (e) cudaEventDestroy(e);
+        // streams: own_stream / own_side / own_copy, after the DevBuf members
     }
 
     void drop_graph() {
@@ -221,6 +268,7 @@ struct tsv_ctx {
     // ------------------------------------------------------------ layout
     void build_layout(uint32_t rows, uint32_t cols, const uint8_t *kinds, const double *dt, size_t ndt,
                       double pitch, double height) {
+        PhaseTimer pt("set_layout");
         ArrayLayout L;
         L.rows = rows;
         L.cols = cols;
@@ -335,6 +383,7 @@ struct tsv_ctx {
         stress.release();
         cudaStream_t s = stream;
         slots.upload(slot_tab.data(), slot_tab.size(), s);
+        glob_of_int_d.upload(node_glob_of_int.data(), node_glob_of_int.size(), s);
         row_cell_d.upload(row_cell.data(), row_cell.size(), s);
         row_kind_d.upload(row_kind.data(), row_kind.size(), s);
         tile_kind_d.upload(tile_kind.data(), tile_kind.size(), s);
@@ -423,6 +472,7 @@ struct tsv_ctx {
 
     // ------------------------------------------------------------------ BC
     void set_bc_mask(std::vector<uint8_t> mask, std::vector<double> vals) {
+        PhaseTimer pt("set_bc_mask");
         constrained = std::move(mask);
         g = std::move(vals);
         any_g = false;
@@ -444,6 +494,16 @@ struct tsv_ctx {
         rhs_dirty = false;
     }
 
+    // Device vector (internal order) -> host array in reference DoF order.
+    void copy_to_reference(const double *v_int, double *out) {
+        uref.alloc(N);
+        to_reference_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), glob_of_int_d.ptr, v_int,
+                                                                    uref.ptr);
+        ++launches;
+        CK(cudaGetLastError());
+        d2h(out, uref.ptr, N * sizeof(double), stream);
+    }
+
     template <typename T>
     std::vector<T> to_internal(const T *v) const {
         std::vector<T> out(N);
@@ -460,20 +520,22 @@ struct tsv_ctx {
     // Assembled load (global_stage.cpp:135-142, cell order, bit-exact) and
     // symmetric lifting (fem.cpp:223-260): b_c = g, b_f -= A_fc g.
     void build_rhs() {
-        std::vector<double> bg(N, 0.0);
-        for (size_t c = 0; c < B; ++c) {
-            const RomHost &m = rom[layout.kind_at(c)];
-            const double dt = layout.delta_t_at(c);
-            const uint32_t *dm = dofmap.data() + c * n;
-            for (size_t a = 0; a < n; ++a) bg[dm[a]] += dt * m.b_el[a];
-        }
-        for (size_t i = 0; i < N; ++i)
-            if (constrained[i]) bg[i] = g[i];
-        std::vector<double> bi = to_internal(bg.data());
-        b.upload(bi.data(), N, stream);
-        if (any_g) {  // b_f -= A_fc g on the device
+        PhaseTimer pt("build_rhs");
+        const RomHost &m0 = rom[0].set ? rom[0] : rom[1];
+        const RomHost &m1 = rom[1].set ? rom[1] : rom[0];
+        DevBuf<double> gd;
+        if (any_g) {
             std::vector<double> gi = to_internal(g.data());
-            r.upload(gi.data(), N, stream);
+            gd.upload(gi.data(), N, stream);
+        }
+        rhs_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), static_cast<int>(n / 3),
+                                                           static_cast<long long>(ldk), slots.ptr, row_cell_d.ptr,
+                                                           row_kind_d.ptr, row_dt_d.ptr, m0.d_bel.ptr, m1.d_bel.ptr,
+                                                           cmask.ptr, any_g ? gd.ptr : nullptr, b.ptr);
+        ++launches;
+        CK(cudaGetLastError());
+        if (any_g) {  // b_f -= A_fc g on the device
+            CK(cudaMemcpyAsync(r.ptr, gd.ptr, N * sizeof(double), cudaMemcpyDeviceToDevice, stream));
             launch_scatter(r.ptr, 2);
             launch_k1(nullptr);
             gather_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), static_cast<int>(n / 3), slots.ptr, cmask.ptr,
@@ -584,11 +646,15 @@ struct tsv_ctx {
             throw StatusError(TSV_ECUDA, "schwarz2: potrf/potri failed");
     }
 
+    SolverHandles solver;  // created on first use, kept for the context's lifetime
+
     void build_schwarz2() {
+        PhaseTimer pt("build_schwarz2");
         const auto t0 = std::chrono::steady_clock::now();
-        SolverHandles h;
-        if (cusolverDnCreate(&h.sol) != CUSOLVER_STATUS_SUCCESS || cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS)
+        if (!solver.sol && (cusolverDnCreate(&solver.sol) != CUSOLVER_STATUS_SUCCESS ||
+                            cublasCreate(&solver.blas) != CUBLAS_STATUS_SUCCESS))
             throw StatusError(TSV_ECUDA, "schwarz2: cuSOLVER/cuBLAS init failed");
+        SolverHandles &h = solver;
         cusolverDnSetStream(h.sol, stream);
         cublasSetStream(h.blas, stream);
         const uint32_t rows = layout.rows, cols = layout.cols;
@@ -1262,6 +1328,7 @@ struct tsv_ctx {
     void ensure_graph() {
         oz_ensure();
         if (iter_graph && graph_oz_s == oz_s) return;
+        PhaseTimer pt("graph capture");
         drop_graph();
         graph_oz_s = oz_s;
         CgParams q = cg_params();
@@ -1281,6 +1348,7 @@ struct tsv_ctx {
         if (!(o.tolerance > 0.0)) throw StatusError(TSV_EINVAL, "IterOptions: tolerance must be > 0");
         if (o.max_iterations < 1) throw StatusError(TSV_EINVAL, "IterOptions: max_iterations must be >= 1");
         if (o.precond < 0 || o.precond > 3) throw StatusError(TSV_EINVAL, "IterOptions: unknown preconditioner");
+        PhaseTimer pt("solve");
         build_precond(o.precond);
         const uint64_t l0 = launches;
         CK(cudaEventRecord(ev0, stream));
@@ -1317,9 +1385,8 @@ struct tsv_ctx {
         last_solve_ms = ms;
         solution_valid = true;
         if (u_out) {
-            std::vector<double> xi(N);
-            d2h(xi.data(), x.ptr, N * sizeof(double), stream);
-            to_reference(xi.data(), u_out);
+            PhaseTimer pt2("u -> host");
+            copy_to_reference(x.ptr, u_out);
         }
         if (info) {
             info->iterations = st.it;
@@ -1499,6 +1566,11 @@ namespace {
 template <typename F>
 int guarded(tsv_ctx *ctx, F &&f) {
     if (!ctx) return TSV_EINVAL;
+    struct AllocScope {
+        cudaStream_t prev;
+        explicit AllocScope(cudaStream_t s) : prev(tl_alloc_stream) { tl_alloc_stream = s; }
+        ~AllocScope() { tl_alloc_stream = prev; }
+    } scope(ctx->stream);
     try {
         int rc = f();
         if (rc == TSV_OK) ctx->err.clear();
@@ -1601,8 +1673,20 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return TSV_ECUDA;
     int rc = guarded(ctx.get(), [&] {
-        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->own_stream.s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->own_side.s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->own_copy.s, cudaStreamNonBlocking));
+        ctx->stream = ctx->own_stream.s;
+        ctx->side = ctx->own_side.s;
+        ctx->copy = ctx->own_copy.s;
+        for (auto &e : ctx->rec_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        {
+            // freed temporaries stay in the pool up to 16 GB (no OS round trip per set-up)
+            cudaMemPool_t pool;
+            CK(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t thr = 16ull << 30;
+            CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        }
         CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
         CK(cudaEventCreate(&ctx->ev0));
@@ -1703,6 +1787,7 @@ int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
         std::memcpy(m.fingerprint, d->fingerprint, 32);
         m.k_r.assign(d->a_element, d->a_element + n * n);
         m.b_el.assign(d->b_element, d->b_element + n);
+        m.d_bel.upload(m.b_el.data(), n, ctx->stream);
         m.u_t.assign(d->thermal, d->thermal + n_fine);
         const size_t ldk = round_up(n, kKC);
         {
@@ -1957,17 +2042,29 @@ int tsv_recover(tsv_ctx *ctx, int points, uint64_t c0, uint64_t c1, double *out)
         if (c0 > c1 || c1 > ctx->B) throw StatusError(TSV_EINVAL, "recover: cell range out of bounds");
         if (c0 == c1) return TSV_OK;
         const size_t per_cell = ctx->elems() * static_cast<size_t>(points) * 7;
-        const size_t max_cells = std::max<size_t>(1, (size_t(2) << 30) / (per_cell * sizeof(double)));
-        DevBuf<double> dout;
+        // Chunks of whole 128-block GEMM tiles (~1 GB), double-buffered: chunk
+        // i+1 is computed on the context stream while chunk i is copied to the
+        // host on the copy stream (the D2H over PCIe is the bound).
+        size_t max_cells = std::max<size_t>(1, (size_t(1) << 30) / (per_cell * sizeof(double)));
+        if (max_cells >= kBM) max_cells = max_cells / kBM * kBM;
+        const size_t stage = std::min(max_cells, static_cast<size_t>(c1 - c0)) * per_cell;
+        for (auto &sb : ctx->rstage)
+            if (sb.count < stage) sb.alloc(stage);
+        cudaEvent_t *computed = ctx->rec_ev, *copied = ctx->rec_ev + 2;
         CK(cudaEventRecord(ctx->ev0, ctx->stream));
-        for (size_t a = c0; a < c1; a += max_cells) {
+        int i = 0;
+        for (size_t a = c0; a < c1; a += max_cells, ++i) {
             const size_t b2 = std::min<size_t>(c1, a + max_cells);
-            dout.alloc((b2 - a) * per_cell);
-            ctx->recover_range(points, a, b2, dout.ptr);
-            CK(cudaMemcpyAsync(out + (a - c0) * per_cell, dout.ptr, (b2 - a) * per_cell * sizeof(double),
-                               cudaMemcpyDeviceToHost, ctx->stream));
-            CK(cudaStreamSynchronize(ctx->stream));
+            const int k = i & 1;
+            if (i >= 2) CK(cudaStreamWaitEvent(ctx->stream, copied[k], 0));
+            ctx->recover_range(points, a, b2, ctx->rstage[k].ptr);
+            CK(cudaEventRecord(computed[k], ctx->stream));
+            CK(cudaStreamWaitEvent(ctx->copy, computed[k], 0));
+            CK(cudaMemcpyAsync(out + (a - c0) * per_cell, ctx->rstage[k].ptr, (b2 - a) * per_cell * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->copy));
+            CK(cudaEventRecord(copied[k], ctx->copy));
         }
+        CK(cudaStreamWaitEvent(ctx->stream, copied[(i - 1) & 1], 0));
         CK(cudaEventRecord(ctx->ev1, ctx->stream));
         CK(cudaEventSynchronize(ctx->ev1));
         float ms = 0.f;

@@ -615,6 +615,53 @@ __global__ void __launch_bounds__(256) cg_scatter_kernel(CgParams q) {
     }
 }
 
+// Assembled thermal load (assemble_global, global_stage.cpp:135-142):
+// b[dof] = sum over the blocks holding dof, in increasing cell order, of
+// dT_cell * b_el[kind][a], each product rounded then added from 0.0 (the
+// reference's sequential loop; no FMA contraction), so b is bit-identical.
+// Constrained DoFs take g (lifting, fem.cpp:223-260; g_int may be NULL = 0).
+__global__ void rhs_kernel(int n_nodes, int nn, long long ldk, const int *slots, const int *row_cell,
+                           const uint8_t *row_kind, const double *row_dt, const double *bel0, const double *bel1,
+                           const uint8_t *cmask, const double *g_int, double *b) {
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= n_nodes) return;
+    const int4 s4 = reinterpret_cast<const int4 *>(slots)[node];
+    const int sl[4] = {s4.x, s4.y, s4.z, s4.w};
+    int cell[4], row[4], rank[4], cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (sl[k] < 0) continue;
+        const int rw = static_cast<int>(sl[k] / ldk);
+        int c = row_cell[rw], q = cnt++;
+        while (q > 0 && cell[q - 1] > c) {  // insertion sort by cell (<= 4 copies)
+            cell[q] = cell[q - 1]; row[q] = row[q - 1]; rank[q] = rank[q - 1];
+            --q;
+        }
+        cell[q] = c;
+        row[q] = rw;
+        rank[q] = static_cast<int>(sl[k] - static_cast<long long>(rw) * ldk);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const long long dof = static_cast<long long>(c) * n_nodes + node;
+        double acc = 0.0;
+        for (int k = 0; k < cnt; ++k) {
+            const double *bel = row_kind[row[k]] ? bel1 : bel0;
+            acc = __dadd_rn(acc, __dmul_rn(row_dt[row[k]], bel[3 * rank[k] + c]));
+        }
+        b[dof] = cmask[dof] ? (g_int ? g_int[dof] : 0.0) : acc;
+    }
+}
+
+// Internal SoA [component][internal node] -> reference DoF order 3 node + c.
+__global__ void to_reference_kernel(int n_nodes, const uint32_t *glob_of_int, const double *v, double *out) {
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= n_nodes) return;
+    const long long g = 3ll * glob_of_int[node];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) out[g + c] = v[static_cast<long long>(c) * n_nodes + node];
+}
+
 // Plain gather/scatter helpers (tsv_apply, recovery, RHS lifting).
 // mode 0: X[slot] = v (free DoFs only, constrained slots zeroed)
 // mode 1: X[slot] = v for every DoF (recovery uses u at all DoFs)
