@@ -89,7 +89,10 @@ struct DevBuf {
         if (n == count && ptr) return;
         release();
         if (n == 0) return;
-        s_ = tl_alloc_stream;
+        // long-lived large buffers (>= 1 GB: stress, U, recovery staging) come
+        // from cudaMalloc: a stream-ordered pool allocation that grows the pool
+        // by tens of GB maps its pages lazily inside the first timed use
+        s_ = n * sizeof(T) >= (size_t(1) << 30) ? nullptr : tl_alloc_stream;
         if (s_) CK(cudaMallocAsync(reinterpret_cast<void **>(&ptr), n * sizeof(T), s_));
         else CK(cudaMalloc(&ptr, n * sizeof(T)));
         count = n;
@@ -215,6 +218,8 @@ struct tsv_ctx {
         DevBuf<double> XL, ZL, z, cellpart, rc, zc, ainv_c, ainv_store;
         DevBuf<const double *> ainv_tab;
         DevBuf<short4> lat;
+        DevBuf<int> node_cell;
+        DevBuf<double4> celltab;
         double setup_ms = 0.0;
         // tensor-core (TF32) local solves
         bool tc = false;
@@ -223,6 +228,10 @@ struct tsv_ctx {
         CUtensorMap tmA{}, tmB{};
         DevBuf<float> ainv_c32;
         int ldc32 = 0;
+        // packed lower tiles of the FP32 inverse (symmetric GEMV, default)
+        DevBuf<float> sym_tiles;
+        DevBuf<double> sym_part;
+        int sym_nt = 0;
     } as2;
     // int8 (Ozaki) K1: digit planes of the X panel
     int oz_s = 0;            // digits per value (0 = DMMA K1)
@@ -689,8 +698,22 @@ struct tsv_ctx {
         }
         as2.lat.upload(lat.data(), lat.size(), stream);
         as2.cell_ptr.upload(node_super_ptr.data(), node_super_ptr.size(), stream);
-        if (partial.count < 2 * static_cast<size_t>(as2.ncells)) partial.alloc(2 * static_cast<size_t>(as2.ncells));
-        as2.cellpart.alloc(static_cast<size_t>(as2.ncells) * 24);
+        {
+            std::vector<int> nc(nodes);
+            std::vector<double4> ct(static_cast<size_t>(as2.ncells));
+            for (int c = 0; c < as2.ncells; ++c) {
+                for (int v = node_super_ptr[c]; v < node_super_ptr[c + 1]; ++v) nc[v] = c;
+                const int x0 = (c % as2.SX) * as2.step, y0 = (c / as2.SX) * as2.step;
+                const int x1 = std::min<int>(x0 + as2.step, static_cast<int>(index.lat_x) - 1);
+                const int y1 = std::min<int>(y0 + as2.step, static_cast<int>(index.lat_y) - 1);
+                ct[c] = make_double4(x0, y0, 1.0 / static_cast<double>(x1 - x0), 1.0 / static_cast<double>(y1 - y0));
+            }
+            as2.node_cell.upload(nc.data(), nc.size(), stream);
+            as2.celltab.upload(ct.data(), ct.size(), stream);
+        }
+        if (partial.count < 2 * static_cast<size_t>(as2.ncells) * kAsSplit)
+            partial.alloc(2 * static_cast<size_t>(as2.ncells) * kAsSplit);
+        as2.cellpart.alloc(static_cast<size_t>(as2.ncells) * kAsSplit * 24);
         as2.rc.alloc(as2.Nc);
         as2.zc.alloc(as2.Nc);
         // Galerkin A_c = sum_b P_b^T K_b P_b (P_b relative to b's super cell,
@@ -792,7 +815,7 @@ struct tsv_ctx {
             spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, cinfo.ptr);
             as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
                                                                                                        as2.Nc);
-            if (!getenv_flag("TSV_AS_COARSE_F64")) {
+            if (!getenv_flag("TSV_AS_COARSE_F64") && getenv_flag("TSV_AS_COARSE_DENSE")) {
                 as2.ldc32 = static_cast<int>(round_up(Ncs, 32));
                 as2.ainv_c32.alloc(Ncs * as2.ldc32);
                 const size_t tot = Ncs * as2.ldc32;
@@ -800,6 +823,19 @@ struct tsv_ctx {
                     as2.ainv_c.ptr, as2.Nc, as2.ldc32, as2.ainv_c32.ptr);
             } else {
                 as2.ainv_c32.release();
+            }
+            if (!getenv_flag("TSV_AS_COARSE_F64") && !getenv_flag("TSV_AS_COARSE_DENSE")) {
+                as2.sym_nt = static_cast<int>((Ncs + kSymT - 1) / kSymT);
+                const long long ntiles = static_cast<long long>(as2.sym_nt) * (as2.sym_nt + 1) / 2;
+                const long long tot = ntiles * kSymT * kSymT;
+                as2.sym_tiles.alloc(static_cast<size_t>(tot));
+                as2.sym_part.alloc(static_cast<size_t>(as2.sym_nt) * as2.sym_nt * kSymT);
+                as_pack_sym_tiles_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
+                    as2.ainv_c.ptr, as2.Nc, as2.sym_tiles.ptr, tot);
+            } else {
+                as2.sym_nt = 0;
+                as2.sym_tiles.release();
+                as2.sym_part.release();
             }
             CK(cudaGetLastError());
         }
@@ -1066,6 +1102,8 @@ struct tsv_ctx {
         a.lat_y = static_cast<int>(index.lat_y);
         a.qm1 = static_cast<int>(nl.n_z - 1);
         a.cell_ptr = as2.cell_ptr.ptr;
+        a.node_cell = as2.node_cell.ptr;
+        a.celltab = as2.celltab.ptr;
         a.ncells = as2.ncells;
         a.cellpart = as2.cellpart.ptr;
         a.rc = as2.rc.ptr;
@@ -1086,15 +1124,25 @@ struct tsv_ctx {
     // coarse solve, prolongation + r.z).
     void launch_as_update_precond(const CgParams &q) {
         AsParams a = as_params();
-        as_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        // r update (grid-stride: a per-cell variant with the restriction fused
+        // in, as_update_kernel<true>, measured 129 us vs 47 + 34 us at config 3:
+        // 110 registers halve the occupancy of a latency-bound stream)
+        as_update_kernel<false><<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
         // fork: the coarse chain (restrict -> coarse rhs -> coarse solve, HBM
         // and latency bound) runs on a side stream beside the local solves
         // (tensor cores); both join before z. Captured as a forked graph.
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(side, ev_fork, 0));
-        as_restrict_kernel<<<as2.ncells, 256, 0, side>>>(q, a);
+        as_restrict_kernel<<<as2.ncells * kAsSplit, 256, 0, side>>>(q, a);
         as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, side>>>(q, a);
-        as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
+        if (as2.sym_nt) {
+            const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
+            as_coarse_symv_kernel<<<ntiles, 128, 0, side>>>(q, a, as2.sym_tiles.ptr, as2.sym_nt, as2.sym_part.ptr);
+            as_coarse_symv_reduce_kernel<<<as2.sym_nt, kSymRedG * kSymT, 0, side>>>(q, a, as2.sym_nt, as2.sym_part.ptr);
+            ++launches;
+        } else {
+            as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
+        }
         CK(cudaEventRecord(ev_join, side));
         if (as2.tc) {
             launch_tc_local();
@@ -1103,7 +1151,7 @@ struct tsv_ctx {
             gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
         }
         CK(cudaStreamWaitEvent(stream, ev_join, 0));
-        as_z_kernel<<<as2.ncells, 256, 0, stream>>>(q, a);
+        as_z_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
         launches += 6;
     }
 
@@ -1322,7 +1370,7 @@ struct tsv_ctx {
     }
 
     int graph_kernels_per_iteration() const {
-        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? 9 : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
+        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? 9 + (as2.sym_nt ? 1 : 0) : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
     }
 
     void ensure_graph() {

@@ -33,6 +33,8 @@ struct AsParams {
     const short4 *lat;     // (gx, gy, gz) lattice position of each internal node
     int step, SX, SY, lat_x, lat_y, qm1;
     const int *cell_ptr;   // super cell -> its contiguous internal node range
+    const int *node_cell;  // internal node -> its super cell
+    const double4 *celltab;  // per super cell: x0, y0, 1/dx, 1/dy (lattice units)
     int ncells;
     double *cellpart;      // [ncells][24]
     double *rc, *zc;       // coarse vectors [Nc]
@@ -56,6 +58,17 @@ __device__ __forceinline__ double round_mantissa(double v, int bits) {
     i += 1LL << (drop - 1);
     i &= ~((1LL << drop) - 1);
     return __longlong_as_double(i);
+}
+
+// Per-cell kernels may run kAsSplit CTAs per super cell, each over a
+// contiguous part of the cell's node range (partials stay per part). Measured
+// on B200 at config 3: splitting by 4 makes both kernels slower (per-CTA
+// reductions and the single completion ticket dominate), so 1.
+constexpr int kAsSplit = 1;  // as_update_kernel<true> assumes one CTA per cell
+__device__ __forceinline__ void as_part_range(const AsParams &a, int cell, int part, int &n0, int &n1) {
+    const int b0 = a.cell_ptr[cell], b1 = a.cell_ptr[cell + 1], len = b1 - b0;
+    n0 = b0 + static_cast<int>((static_cast<long long>(len) * part) / kAsSplit);
+    n1 = b0 + static_cast<int>((static_cast<long long>(len) * (part + 1)) / kAsSplit);
 }
 
 // Trilinear weights of a node relative to super cell (cx, cy). Nodes are
@@ -99,16 +112,40 @@ __device__ __forceinline__ int as_corner_node(const AsParams &a, int cx, int cy,
 // r scattered into the local-solve panel; r.r reduced; the last CTA runs
 // the loop-head bookkeeping of cg_solve (iteration count, best iterate,
 // max-iteration exit, next product = A x when the residual test passes).
+//
+// kCell: one CTA per super cell over its contiguous node range, with the
+// coarse restriction P^T r fused in (the cell's 24 partials, the same
+// weights as_z_kernel prolongs with), so the coarse chain starts at the
+// coarse right-hand side.
+template <bool kCell>
 __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) {
     __shared__ double sh[64];
+    __shared__ double shr[8][24];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int phase = st->phase;
     const double alpha = st->alpha;
     const int N = q.n_nodes;
     double part[1] = {0.0};
-    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+    double acc[kCell ? 24 : 1];
+#pragma unroll
+    for (int k = 0; k < (kCell ? 24 : 1); ++k) acc[k] = 0.0;
+    int n_begin, n_end, n_step;
+    AsCell cc{};
+    if (kCell) {
+        cc = as_cell(a, blockIdx.x);
+        n_begin = a.cell_ptr[blockIdx.x] + threadIdx.x;
+        n_end = a.cell_ptr[blockIdx.x + 1];
+        n_step = blockDim.x;
+    } else {
+        n_begin = blockIdx.x * blockDim.x + threadIdx.x;
+        n_end = N;
+        n_step = gridDim.x * blockDim.x;
+    }
+    for (int node = n_begin; node < n_end; node += n_step) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+        double w[8];
+        if (kCell) as_cell_weights(a, cc, node, w);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
@@ -126,6 +163,10 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             }
             part[0] += rv * rv;
             if (q.cmask[dof]) continue;
+            if (kCell) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[(3 * k + c) % (kCell ? 24 : 1)] += w[k] * rv;
+            }
             const int co = c * q.nn;
             if (a.XL32) {
                 const float f = to_tf32(rv);
@@ -140,6 +181,20 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
                 if (s.z >= 0) a.XL[s.z + co] = rv;
                 if (s.w >= 0) a.XL[s.w + co] = rv;
             }
+        }
+    }
+    if (kCell) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int k = 0; k < (kCell ? 24 : 1); ++k) {
+            const double v = warp_sum(acc[k]);
+            if (lane == 0) shr[warp][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < 24) {
+            double t = 0.0;
+            for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) t += shr[w2][threadIdx.x];
+            a.cellpart[blockIdx.x * 24 + threadIdx.x] = t;
         }
     }
     block_sum<1>(part, sh);
@@ -188,16 +243,18 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
 
 // Restriction, one CTA per super cell over its contiguous node range: the
 // cell's 24 partials of P^T r.
-__global__ void __launch_bounds__(256, 3) as_restrict_kernel(CgParams q, AsParams a) {
+__global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a) {
     __shared__ double sh[8][24];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int N = q.n_nodes;
-    const int cell = blockIdx.x;
+    const int cell = blockIdx.x / kAsSplit;
     const AsCell cc = as_cell(a, cell);
+    int nb, ne;
+    as_part_range(a, cell, blockIdx.x % kAsSplit, nb, ne);
     double acc[24];
 #pragma unroll
     for (int k = 0; k < 24; ++k) acc[k] = 0.0;
-    for (int node = a.cell_ptr[cell] + threadIdx.x; node < a.cell_ptr[cell + 1]; node += blockDim.x) {
+    for (int node = nb + threadIdx.x; node < ne; node += blockDim.x) {
         double w[8];
         as_cell_weights(a, cc, node, w);
 #pragma unroll
@@ -218,7 +275,7 @@ __global__ void __launch_bounds__(256, 3) as_restrict_kernel(CgParams q, AsParam
     if (threadIdx.x < 24) {
         double t = 0.0;
         for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) t += sh[w2][threadIdx.x];
-        a.cellpart[cell * 24 + threadIdx.x] = t;
+        a.cellpart[blockIdx.x * 24 + threadIdx.x] = t;  // [cell][part][24]
     }
 }
 
@@ -236,7 +293,8 @@ __global__ void as_coarse_rhs_kernel(CgParams q, AsParams a) {
         for (int cx = gx - 1; cx <= gx; ++cx) {
             if (cx < 0 || cx >= a.SX) continue;
             const int corner = (gx - cx) | ((gy - cy) << 1) | (gz << 2);
-            s += a.cellpart[(cy * a.SX + cx) * 24 + 3 * corner + comp];
+            for (int part = 0; part < kAsSplit; ++part)
+                s += a.cellpart[((cy * a.SX + cx) * kAsSplit + part) * 24 + 3 * corner + comp];
         }
     }
     a.rc[j] = s;
@@ -289,25 +347,129 @@ __global__ void __launch_bounds__(256) as_coarse_gemv_kernel(CgParams q, AsParam
     }
 }
 
-// Z, one CTA per super cell: z = sum of local products (owner gather) +
-// P zc (the cell's 24 coarse values staged in shared memory); (r.z)
-// reduced; the last CTA sets beta / rho (p = z + beta p, or p = z after
-// init/restart).
+// Coarse solve on the packed lower triangle of the symmetric FP32 inverse
+// (half the HBM stream of the dense GEMV). Tile (I, J), I >= J, of
+// kSymT x kSymT is stored contiguously; its CTA writes the partial
+// A_IJ rc_J to part[I][J] and (I != J) A_IJ^T rc_I to part[J][I]; the
+// reduction sums part[I][0..NT) in order (fixed order: deterministic).
+constexpr int kSymT = 64;
+
+__device__ __forceinline__ void sym_tile_of(int t, int &I, int &J) {
+    // t enumerates lower tiles row by row: t = I (I + 1) / 2 + J
+    I = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    J = t - I * (I + 1) / 2;
+}
+
+__global__ void __launch_bounds__(128) as_coarse_symv_kernel(CgParams q, AsParams a, const float *tiles, int NT,
+                                                             double *part) {
+    __shared__ double xi[kSymT], xj[kSymT];
+    __shared__ double colp[8][kSymT];
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    int I, J;
+    sym_tile_of(blockIdx.x, I, J);
+    const int t = threadIdx.x;
+    if (t < kSymT) {
+        const int gi = I * kSymT + t, gj = J * kSymT + t;
+        xi[t] = gi < a.Nc ? a.rc[gi] : 0.0;
+        xj[t] = gj < a.Nc ? a.rc[gj] : 0.0;
+    }
+    // thread t holds rows t/16 + 8k (k = 0..7), columns 4 (t % 16) .. + 3
+    const float4 *src = reinterpret_cast<const float4 *>(tiles + static_cast<long long>(blockIdx.x) * kSymT * kSymT);
+    float4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(src + t + 128 * k);
+    __syncthreads();
+    const int c0 = 4 * (t & 15), r0 = t >> 4;
+    double cs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int row = r0 + 8 * k;
+        double rs = static_cast<double>(v[k].x) * xj[c0] + static_cast<double>(v[k].y) * xj[c0 + 1] +
+                    static_cast<double>(v[k].z) * xj[c0 + 2] + static_cast<double>(v[k].w) * xj[c0 + 3];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);  // 16 lanes share a row
+        if ((t & 15) == 0) part[(static_cast<long long>(I) * NT + J) * kSymT + row] = rs;
+        const double xr = xi[row];
+        cs[0] += static_cast<double>(v[k].x) * xr;
+        cs[1] += static_cast<double>(v[k].y) * xr;
+        cs[2] += static_cast<double>(v[k].z) * xr;
+        cs[3] += static_cast<double>(v[k].w) * xr;
+    }
+    if (I == J) return;
+    // column sums: reduce over the 8 row groups r0 (lanes 16 apart, then warps)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cs[c] += __shfl_xor_sync(0xffffffffu, cs[c], 16);
+    const int warp = t >> 5;
+    if ((t & 16) == 0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) colp[warp][c0 + c] = cs[c];
+    __syncthreads();
+    if (t < kSymT) {
+        const double s = (colp[0][t] + colp[1][t]) + (colp[2][t] + colp[3][t]);
+        part[(static_cast<long long>(J) * NT + I) * kSymT + t] = s;
+    }
+}
+
+// zc[I*T + r] = sum_J part[I][J][r], J in order: a CTA of 16 x 64 threads per
+// block row I; thread group g sums J = g, g + 16, ... and the 16 group sums
+// are added in group order (fixed order: deterministic).
+constexpr int kSymRedG = 16;
+__global__ void __launch_bounds__(kSymRedG * kSymT) as_coarse_symv_reduce_kernel(CgParams q, AsParams a, int NT,
+                                                                               const double *part) {
+    __shared__ double sh[kSymRedG][kSymT];
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    const int I = blockIdx.x, r = threadIdx.x % kSymT, grp = threadIdx.x / kSymT;
+    double s = 0.0;
+    for (int J = grp; J < NT; J += kSymRedG) s += part[(static_cast<long long>(I) * NT + J) * kSymT + r];
+    sh[grp][r] = s;
+    __syncthreads();
+    if (grp == 0) {
+        double t = 0.0;
+#pragma unroll
+        for (int g = 0; g < kSymRedG; ++g) t += sh[g][r];
+        const int i = I * kSymT + r;
+        if (i < a.Nc) a.zc[i] = t;
+    }
+}
+
+// Pack the lower tiles of the full symmetric FP64 inverse (column-major) as FP32.
+__global__ void as_pack_sym_tiles_kernel(const double *A, int Nc, float *tiles, long long total) {
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int t = static_cast<int>(e / (kSymT * kSymT)), w = static_cast<int>(e % (kSymT * kSymT));
+    int I, J;
+    sym_tile_of(t, I, J);
+    const int row = I * kSymT + w / kSymT, col = J * kSymT + w % kSymT;
+    tiles[e] = (row < Nc && col < Nc) ? static_cast<float>(A[static_cast<long long>(col) * Nc + row]) : 0.0f;
+}
+
+// Z, grid-stride over nodes (fixed grid, like the other vector kernels: a
+// CTA per super cell ran at half the occupancy): z = sum of local products
+// (owner gather) + P zc (the node's cell from node_cell, its corner
+// geometry from celltab); (r.z) reduced; the last CTA sets beta / rho
+// (p = z + beta p, or p = z after init/restart).
 __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
     __shared__ double sh[64];
-    __shared__ double zc[24];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int N = q.n_nodes;
-    const int cell = blockIdx.x;
-    const AsCell cc = as_cell(a, cell);
-    if (threadIdx.x < 24) zc[threadIdx.x] = a.zc[3 * as_corner_node(a, cc.cx, cc.cy, threadIdx.x / 3) + threadIdx.x % 3];
-    __syncthreads();
+    const double rdz = 1.0 / static_cast<double>(a.qm1);
     double part[1] = {0.0};
-    for (int node = a.cell_ptr[cell] + threadIdx.x; node < a.cell_ptr[cell + 1]; node += blockDim.x) {
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+        const int cell = a.node_cell[node];
+        const double4 ct = a.celltab[cell];  // x0, y0, 1/dx, 1/dy
+        const short4 L = a.lat[node];
+        const double tx = (static_cast<double>(L.x) - ct.x) * ct.z;
+        const double ty = (static_cast<double>(L.y) - ct.y) * ct.w;
+        const double tz = static_cast<double>(L.z) * rdz;
         double w[8];
-        as_cell_weights(a, cc, node, w);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            w[k] = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
+        const int cx = cell % a.SX, cy = cell / a.SX;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
@@ -330,7 +492,7 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
                     if (s.w >= 0) zv += a.ZL[s.w + co];
                 }
 #pragma unroll
-                for (int k = 0; k < 8; ++k) zv += w[k] * zc[3 * k + c];
+                for (int k = 0; k < 8; ++k) zv += w[k] * __ldg(a.zc + 3 * as_corner_node(a, cx, cy, k) + c);
             }
             a.z[dof] = zv;
             part[0] += rv * zv;
