@@ -230,7 +230,7 @@ struct tsv_ctx {
         int ldc32 = 0;
         // packed lower tiles of the FP32 inverse (symmetric GEMV, default)
         DevBuf<float> sym_tiles;
-        DevBuf<double> sym_part;
+        DevBuf<double> sym_part, dotpart;
         int sym_nt = 0;
     } as2;
     // int8 (Ozaki) K1: digit planes of the X panel
@@ -830,6 +830,7 @@ struct tsv_ctx {
                 const long long tot = ntiles * kSymT * kSymT;
                 as2.sym_tiles.alloc(static_cast<size_t>(tot));
                 as2.sym_part.alloc(static_cast<size_t>(as2.sym_nt) * as2.sym_nt * kSymT);
+                as2.dotpart.alloc(static_cast<size_t>(as2.sym_nt));
                 as_pack_sym_tiles_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
                     as2.ainv_c.ptr, as2.Nc, as2.sym_tiles.ptr, tot);
             } else {
@@ -1107,6 +1108,7 @@ struct tsv_ctx {
         a.ncells = as2.ncells;
         a.cellpart = as2.cellpart.ptr;
         a.rc = as2.rc.ptr;
+        a.dotpart = as2.dotpart.ptr;
         a.zc = as2.zc.ptr;
         a.ainv_c = as2.ainv_c.ptr;
         a.ainv_c32 = as2.ainv_c32.ptr;
@@ -1124,13 +1126,14 @@ struct tsv_ctx {
     // coarse solve, prolongation + r.z).
     void launch_as_update_precond(const CgParams &q) {
         AsParams a = as_params();
-        // r update (grid-stride: a per-cell variant with the restriction fused
-        // in, as_update_kernel<true>, measured 129 us vs 47 + 34 us at config 3:
-        // 110 registers halve the occupancy of a latency-bound stream)
-        as_update_kernel<false><<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
-        // fork: the coarse chain (restrict -> coarse rhs -> coarse solve, HBM
-        // and latency bound) runs on a side stream beside the local solves
-        // (tensor cores); both join before z. Captured as a forked graph.
+        // r update (grid-stride). Fusing the coarse restriction in (warp-level
+        // per-cell partials) measured slower at config 3: 80 us vs 47 + 34 us
+        // with the restriction off the critical path on the side stream.
+        as_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        // fork: the coarse chain (cell sums of the restriction -> coarse rhs
+        // -> coarse solve, HBM and latency bound) runs on a side stream beside
+        // the local solves (tensor cores); both join before z. Captured as a
+        // forked graph.
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(side, ev_fork, 0));
         as_restrict_kernel<<<as2.ncells * kAsSplit, 256, 0, side>>>(q, a);
@@ -1139,9 +1142,9 @@ struct tsv_ctx {
             const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
             as_coarse_symv_kernel<<<ntiles, 128, 0, side>>>(q, a, as2.sym_tiles.ptr, as2.sym_nt, as2.sym_part.ptr);
             as_coarse_symv_reduce_kernel<<<as2.sym_nt, kSymRedG * kSymT, 0, side>>>(q, a, as2.sym_nt, as2.sym_part.ptr);
-            ++launches;
         } else {
             as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
+            as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
         }
         CK(cudaEventRecord(ev_join, side));
         if (as2.tc) {
@@ -1150,9 +1153,21 @@ struct tsv_ctx {
             GemmParams gp = local_gemm_params();
             gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
         }
+        // the local part of z (and r.z_l) while the coarse chain finishes
+        as_zl_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
         CK(cudaStreamWaitEvent(stream, ev_join, 0));
-        as_z_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
-        launches += 6;
+        launches += 7;
+    }
+
+    // C: p update + next operand panel (Schwarz: adds the coarse part of z).
+    void launch_scatter_p(const CgParams &q, int write_z = 0) {
+        if (pre_kind == TSV_PRECOND_SCHWARZ2) {
+            AsParams a = as_params();
+            as_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a, write_z);
+        } else {
+            cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        }
+        ++launches;
     }
 
     // ------------------------------------------------------------ kernels
@@ -1365,12 +1380,12 @@ struct tsv_ctx {
             cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
             ++launches;
         }
-        cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
-        launches += 2;
+        launch_scatter_p(q);
+        ++launches;
     }
 
     int graph_kernels_per_iteration() const {
-        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? 9 + (as2.sym_nt ? 1 : 0) : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
+        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? 10 : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
     }
 
     void ensure_graph() {
@@ -1473,8 +1488,7 @@ struct tsv_ctx {
             cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
             ++launches;
         }
-        cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
-        ++launches;
+        launch_scatter_p(q);
         CK(cudaGetLastError());
         // Host-polled batches of graph-captured iterations; a finished
         // solve turns the remaining launches into early exits.
@@ -2015,6 +2029,7 @@ int tsv_precond_apply(tsv_ctx *ctx, int precond, const double *r_in, double *z_o
         CK(cudaMemcpyAsync(ctx->state.ptr, ctx->h_state, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
         CgParams q = ctx->cg_params();
         ctx->launch_as_update_precond(q);
+        ctx->launch_scatter_p(q, 1);  // z = z_l + P zc (p / panel updates are discarded)
         CK(cudaGetLastError());
         std::vector<double> zi(ctx->N);
         CK(cudaMemcpyAsync(zi.data(), ctx->as2.z.ptr, ctx->N * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

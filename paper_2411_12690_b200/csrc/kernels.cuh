@@ -331,7 +331,8 @@ struct CgState {
     int p_assign;   // 1: p = z (fresh start), 0: p = z + beta p
     int it, best_it, max_it, breakdown_code, restarts;
     double rho, alpha, beta, res, best_res, norm_b, tol, tol_abs;
-    unsigned ticket_a, ticket_b;
+    double rz_l, rz_c;  // Schwarz: r.z split into the local part and (P^T r).zc
+    unsigned ticket_a, ticket_b, ticket_c;  // c: side-stream kernels
 };
 
 // Device vectors are structure-of-arrays per component: DoF (node, c) of

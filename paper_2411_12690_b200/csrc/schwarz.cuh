@@ -38,6 +38,7 @@ struct AsParams {
     int ncells;
     double *cellpart;      // [ncells][24]
     double *rc, *zc;       // coarse vectors [Nc]
+    double *dotpart;       // [sym_nt] partials of rc.zc (symmetric coarse path)
     const double *ainv_c;  // dense [Nc][Nc]
     const float *ainv_c32; // FP32 copy [Nc][ldc32] (default; TSV_AS_COARSE_F64 keeps FP64): halves the
                            // coarse HBM stream. With the FP64 DMMA true-residual check it raised the
@@ -112,40 +113,17 @@ __device__ __forceinline__ int as_corner_node(const AsParams &a, int cx, int cy,
 // r scattered into the local-solve panel; r.r reduced; the last CTA runs
 // the loop-head bookkeeping of cg_solve (iteration count, best iterate,
 // max-iteration exit, next product = A x when the residual test passes).
-//
-// kCell: one CTA per super cell over its contiguous node range, with the
-// coarse restriction P^T r fused in (the cell's 24 partials, the same
-// weights as_z_kernel prolongs with), so the coarse chain starts at the
-// coarse right-hand side.
-template <bool kCell>
+
 __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) {
     __shared__ double sh[64];
-    __shared__ double shr[8][24];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int phase = st->phase;
     const double alpha = st->alpha;
     const int N = q.n_nodes;
     double part[1] = {0.0};
-    double acc[kCell ? 24 : 1];
-#pragma unroll
-    for (int k = 0; k < (kCell ? 24 : 1); ++k) acc[k] = 0.0;
-    int n_begin, n_end, n_step;
-    AsCell cc{};
-    if (kCell) {
-        cc = as_cell(a, blockIdx.x);
-        n_begin = a.cell_ptr[blockIdx.x] + threadIdx.x;
-        n_end = a.cell_ptr[blockIdx.x + 1];
-        n_step = blockDim.x;
-    } else {
-        n_begin = blockIdx.x * blockDim.x + threadIdx.x;
-        n_end = N;
-        n_step = gridDim.x * blockDim.x;
-    }
-    for (int node = n_begin; node < n_end; node += n_step) {
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
-        double w[8];
-        if (kCell) as_cell_weights(a, cc, node, w);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
@@ -163,10 +141,6 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             }
             part[0] += rv * rv;
             if (q.cmask[dof]) continue;
-            if (kCell) {
-#pragma unroll
-                for (int k = 0; k < 8; ++k) acc[(3 * k + c) % (kCell ? 24 : 1)] += w[k] * rv;
-            }
             const int co = c * q.nn;
             if (a.XL32) {
                 const float f = to_tf32(rv);
@@ -181,20 +155,6 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
                 if (s.z >= 0) a.XL[s.z + co] = rv;
                 if (s.w >= 0) a.XL[s.w + co] = rv;
             }
-        }
-    }
-    if (kCell) {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int k = 0; k < (kCell ? 24 : 1); ++k) {
-            const double v = warp_sum(acc[k]);
-            if (lane == 0) shr[warp][k] = v;
-        }
-        __syncthreads();
-        if (threadIdx.x < 24) {
-            double t = 0.0;
-            for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) t += shr[w2][threadIdx.x];
-            a.cellpart[blockIdx.x * 24 + threadIdx.x] = t;
         }
     }
     block_sum<1>(part, sh);
@@ -419,18 +379,34 @@ constexpr int kSymRedG = 16;
 __global__ void __launch_bounds__(kSymRedG * kSymT) as_coarse_symv_reduce_kernel(CgParams q, AsParams a, int NT,
                                                                                const double *part) {
     __shared__ double sh[kSymRedG][kSymT];
+    __shared__ double shd[64];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int I = blockIdx.x, r = threadIdx.x % kSymT, grp = threadIdx.x / kSymT;
     double s = 0.0;
     for (int J = grp; J < NT; J += kSymRedG) s += part[(static_cast<long long>(I) * NT + J) * kSymT + r];
     sh[grp][r] = s;
     __syncthreads();
+    // rc.zc folded in: this block row's partial, then the last CTA (ticket_c)
+    // sums the partials in CTA order
+    double d[1] = {0.0};
     if (grp == 0) {
         double t = 0.0;
 #pragma unroll
         for (int g = 0; g < kSymRedG; ++g) t += sh[g][r];
         const int i = I * kSymT + r;
-        if (i < a.Nc) a.zc[i] = t;
+        if (i < a.Nc) {
+            a.zc[i] = t;
+            d[0] = a.rc[i] * t;
+        }
+    }
+    block_sum<1>(d, shd);
+    if (!publish_partials<1>(d, a.dotpart, &q.st->ticket_c)) return;
+    double tot[1];
+    grid_sum<1>(a.dotpart, gridDim.x, tot, shd);
+    if (threadIdx.x == 0) {
+        q.st->ticket_c = 0u;
+        q.st->rz_c = tot[0];
+        __threadfence();
     }
 }
 
@@ -445,31 +421,22 @@ __global__ void as_pack_sym_tiles_kernel(const double *A, int Nc, float *tiles, 
     tiles[e] = (row < Nc && col < Nc) ? static_cast<float>(A[static_cast<long long>(col) * Nc + row]) : 0.0f;
 }
 
-// Z, grid-stride over nodes (fixed grid, like the other vector kernels: a
-// CTA per super cell ran at half the occupancy): z = sum of local products
-// (owner gather) + P zc (the node's cell from node_cell, its corner
-// geometry from celltab); (r.z) reduced; the last CTA sets beta / rho
-// (p = z + beta p, or p = z after init/restart).
-__global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
+// The preconditioned residual is z = z_l + P zc, with z_l the local part
+// (owner gather of the local products; z = r on constrained DoFs) and P zc
+// the coarse part (free DoFs). Since P^T r (free DoFs) is the coarse
+// right-hand side rc, r.z = r.z_l + rc.zc: the local kernel (as_zl) runs on
+// the main stream while the coarse chain finishes on the side stream, and
+// the coarse part is added where z is consumed (as_scatter_kernel).
+
+// z_l and r.z_l (grid-stride, fixed grid; the last CTA stores rz_l).
+__global__ void __launch_bounds__(256) as_zl_kernel(CgParams q, AsParams a) {
     __shared__ double sh[64];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int N = q.n_nodes;
-    const double rdz = 1.0 / static_cast<double>(a.qm1);
     double part[1] = {0.0};
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
-        const int cell = a.node_cell[node];
-        const double4 ct = a.celltab[cell];  // x0, y0, 1/dx, 1/dy
-        const short4 L = a.lat[node];
-        const double tx = (static_cast<double>(L.x) - ct.x) * ct.z;
-        const double ty = (static_cast<double>(L.y) - ct.y) * ct.w;
-        const double tz = static_cast<double>(L.z) * rdz;
-        double w[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            w[k] = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
-        const int cx = cell % a.SX, cy = cell / a.SX;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
@@ -491,8 +458,6 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
                     if (s.z >= 0) zv += a.ZL[s.z + co];
                     if (s.w >= 0) zv += a.ZL[s.w + co];
                 }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) zv += w[k] * __ldg(a.zc + 3 * as_corner_node(a, cx, cy, k) + c);
             }
             a.z[dof] = zv;
             part[0] += rv * zv;
@@ -504,16 +469,84 @@ __global__ void __launch_bounds__(256) as_z_kernel(CgParams q, AsParams a) {
     grid_sum<1>(q.partial, gridDim.x, tot, sh);
     if (threadIdx.x != 0) return;
     st->ticket_a = 0u;
-    const double rz = tot[0];
-    if (st->phase == PH_NORMAL) {
-        st->beta = rz / st->rho;
-        st->rho = rz;
+    st->rz_l = tot[0];
+    __threadfence();
+}
+
+// rc.zc on the side stream (one CTA, fixed order).
+__global__ void __launch_bounds__(1024) as_coarse_dot_kernel(CgParams q, AsParams a) {
+    __shared__ double sh[64];
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    double v[1] = {0.0};
+    for (int i = threadIdx.x; i < a.Nc; i += blockDim.x) v[0] += a.rc[i] * a.zc[i];
+    block_sum<1>(v, sh);
+    if (threadIdx.x == 0) q.st->rz_c = v[0];
+}
+
+// p = z + beta p (or p = z after init/restart) with z = z_l + P zc, beta =
+// (rz_l + rz_c) / rho; the next operator operand (p, or x for a
+// verification) goes into the block-major panel (free DoFs). The last CTA
+// advances rho / phase. With write_z (tsv_precond_apply) z is stored too.
+__global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a, int write_z) {
+    __shared__ bool last;
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int yx = st->y_holds_x;
+    const bool normal = st->phase == PH_NORMAL;
+    const double rz = st->rz_l + st->rz_c;
+    const double beta = normal ? rz / st->rho : 0.0;
+    const int N = q.n_nodes;
+    const double rdz = 1.0 / static_cast<double>(a.qm1);
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+        const int cell = a.node_cell[node];
+        const double4 ct = a.celltab[cell];
+        const short4 L = a.lat[node];
+        const double tx = (static_cast<double>(L.x) - ct.x) * ct.z;
+        const double ty = (static_cast<double>(L.y) - ct.y) * ct.w;
+        const double tz = static_cast<double>(L.z) * rdz;
+        const int cx = cell % a.SX, cy = cell / a.SX;
+        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            double zv = a.z[dof];
+            const bool cm = q.cmask[dof] != 0;
+            if (!cm) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
+                    zv += w * __ldg(a.zc + 3 * as_corner_node(a, cx, cy, k) + c);
+                }
+            }
+            if (write_z) a.z[dof] = zv;
+            const double pn = normal ? zv + beta * q.p[dof] : zv;
+            q.p[dof] = pn;
+            if (cm) continue;
+            const double v = yx ? q.x[dof] : pn;
+            const int co = c * q.nn;
+            if (s.x >= 0) q.X[s.x + co] = v;
+            if (s.y >= 0) q.X[s.y + co] = v;
+            if (s.z >= 0) q.X[s.z + co] = v;
+            if (s.w >= 0) q.X[s.w + co] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&st->ticket_b, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    st->ticket_b = 0u;
+    if (normal) {
+        st->beta = beta;
         st->p_assign = 0;
-    } else {  // INIT or RESTART: p = z
-        st->rho = rz;
+    } else {
         st->p_assign = 1;
         st->phase = PH_NORMAL;
     }
+    st->rho = rz;
     __threadfence();
 }
 
