@@ -8,14 +8,14 @@ import sys
 
 rows = [r for r in csv.DictReader(l for l in open(sys.argv[1]) if not l.startswith("=="))
         if r["Metric Name"] == "gpu__time_duration.sum"]
-stress = [i for i, r in enumerate(rows) if r["Kernel Name"].startswith("tsvb200::stress_kernel")]
+stress = [i for i, r in enumerate(rows) if "stress_kernel" in r["Kernel Name"]]
 end = stress[-1]
 prev = [i for i in stress if i < end]
 # step boundary: the previous step's last stress launch (followed by a solver kernel)
 start = 0
 for i in reversed(prev):
     nxt = rows[i + 1]["Kernel Name"]
-    if not (nxt.startswith("tsvb200::stress_kernel") or "gemm_nt_f64" in nxt or "scatter_vec" in nxt):
+    if not ("stress_kernel" in nxt or "gemm_nt_f64" in nxt or "scatter_vec" in nxt):
         start = i + 1
         break
 acc = collections.OrderedDict()
