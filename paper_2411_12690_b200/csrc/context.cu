@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <exception>
 #include <vector>
 
 #include "../../include/tsv_b200.h"
@@ -108,12 +109,18 @@ struct PhaseTimer {
     const char *name;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     explicit PhaseTimer(const char *n) : name(n) {}
-    ~PhaseTimer() {
+    void report() const {
         static const bool on = [] { const char *v = std::getenv("TSV_TIMING"); return v && *v && *v != '0'; }();
         if (on)
             std::fprintf(stderr, "[tsv timing] %-22s %8.2f ms\n", name,
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     }
+    void lap(const char *next) {  // report this phase, start the next
+        report();
+        name = next;
+        t0 = std::chrono::steady_clock::now();
+    }
+    ~PhaseTimer() { report(); }
 };
 
 // Owns a stream; declared first in tsv_ctx so it is destroyed after every
@@ -230,7 +237,7 @@ struct tsv_ctx {
         int ldc32 = 0;
         // packed lower tiles of the FP32 inverse (symmetric GEMV, default)
         DevBuf<float> sym_tiles;
-        DevBuf<double> sym_part, dotpart;
+        DevBuf<double> sym_part, dotpart, kcell_d, cwork;
         int sym_nt = 0;
     } as2;
     // int8 (Ozaki) K1: digit planes of the X panel
@@ -302,8 +309,14 @@ struct tsv_ctx {
 
         layout = L;
         nl = NodeLayout::create(m.q[0], m.q[1], m.q[2]);
-        index = index_global_nodes(layout, nl);
-        dofmap = tsvb200::dof_map(layout, index, nl);
+        {
+            PhaseTimer pt1("  index_global_nodes");
+            index = index_global_nodes(layout, nl);
+        }
+        {
+            PhaseTimer pt1("  dof_map");
+            dofmap = tsvb200::dof_map(layout, index, nl);
+        }
         n = nl.reduced_dofs();
         ldk = round_up(n, kKC);
         B = layout.cell_count();
@@ -342,6 +355,7 @@ struct tsv_ctx {
         k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(k1_grid);  // fewer tiles than CTA slots
         setup_streamk();
 
+        PhaseTimer pt_ren("  renumber+slots");
         // Node renumbering (first visit, blocks in super-cell-major order:
         // the nodes of each Schwarz super cell form one contiguous range)
         // + slot table.
@@ -385,6 +399,7 @@ struct tsv_ctx {
         }
         if (node_glob_of_int.size() != nodes) throw StatusError(TSV_EINVAL, "index: unreferenced global node");
 
+        pt_ren.lap("  uploads");
         drop_graph();
         solution_valid = false;
         pre_kind = -1;
@@ -439,7 +454,7 @@ struct tsv_ctx {
         // (deterministic choice: results stay bitwise reproducible).
         const double rounds = std::ceil(static_cast<double>(T) / static_cast<double>(G));
         const double eff = (C / (static_cast<double>(KC) * static_cast<double>(fpt))) / (rounds * static_cast<double>(G));
-        if (eff > 0.88) return;
+        if (eff > 0.88 && !getenv_flag("TSV_STREAMK")) return;
         std::vector<int> start(G + 1, 0);
         size_t it = 0;
         double cum = 0.0;
@@ -655,7 +670,8 @@ struct tsv_ctx {
             throw StatusError(TSV_ECUDA, "schwarz2: potrf/potri failed");
     }
 
-    SolverHandles solver;  // created on first use, kept for the context's lifetime
+    SolverHandles solver;   // created on first use, kept for the context's lifetime
+    SolverHandles solver2;  // the coarse inverse's (worker thread, side stream)
 
     void build_schwarz2() {
         PhaseTimer pt("build_schwarz2");
@@ -668,10 +684,10 @@ struct tsv_ctx {
         cublasSetStream(h.blas, stream);
         const uint32_t rows = layout.rows, cols = layout.cols;
         const size_t nn = n / 3;
-        const bool dbg = getenv_flag("TSV_DEBUG");
-        auto tick = [&](const char *what) {
+        const bool dbg = getenv_flag("TSV_DEBUG"), timing = getenv_flag("TSV_TIMING");
+        auto tick = [&](const char *what) {  // TSV_DEBUG: device-synchronised; TSV_TIMING: host time only
             if (dbg) cudaStreamSynchronize(stream);
-            if (dbg)
+            if (dbg || timing)
                 std::fprintf(stderr, "[schwarz2] %-28s %8.1f ms\n", what,
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         };
@@ -799,47 +815,82 @@ struct tsv_ctx {
             }
         tick("coarse Galerkin products");
         const size_t Ncs = static_cast<size_t>(as2.Nc);
+        // The dense coarse inverse (cuSOLVER potrf + potri on Nc ~ 7e3, whose
+        // host-side enqueue alone blocks for ~30 ms) runs on a worker thread
+        // on the side stream while this thread builds the local stage. Device
+        // buffers are allocated here, on the context stream, before the fork.
+        const bool coarse_f64 = getenv_flag("TSV_AS_COARSE_F64"), coarse_dense = getenv_flag("TSV_AS_COARSE_DENSE");
         as2.ainv_c.alloc(Ncs * Ncs);
         CK(cudaMemsetAsync(as2.ainv_c.ptr, 0, Ncs * Ncs * sizeof(double), stream));
-        {
-            DevBuf<double> dk;
-            dk.upload(kcell.data(), kcell.size(), stream);
-            for (int py = 0; py < 2; ++py)
-                for (int px = 0; px < 2; ++px) {
-                    const long long cnt = static_cast<long long>((as2.SX - px + 1) / 2) * ((as2.SY - py + 1) / 2) * 576;
-                    if (cnt <= 0) continue;
-                    as_coarse_scatter_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, stream>>>(
-                        dk.ptr, as2.SX, as2.SY, px, py, as2.ainv_c.ptr, as2.Nc);
-                }
-            as_fix_zero_rows_kernel<<<static_cast<unsigned>((Ncs + 7) / 8), 256, 0, stream>>>(as2.ainv_c.ptr, as2.Nc);
-            spd_inverse_inplace(h, as2.ainv_c.ptr, as2.Nc, work, cinfo.ptr);
-            as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, stream>>>(as2.ainv_c.ptr,
-                                                                                                       as2.Nc);
-            if (!getenv_flag("TSV_AS_COARSE_F64") && getenv_flag("TSV_AS_COARSE_DENSE")) {
-                as2.ldc32 = static_cast<int>(round_up(Ncs, 32));
-                as2.ainv_c32.alloc(Ncs * as2.ldc32);
-                const size_t tot = Ncs * as2.ldc32;
-                as_coarse_to_f32_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
-                    as2.ainv_c.ptr, as2.Nc, as2.ldc32, as2.ainv_c32.ptr);
-            } else {
-                as2.ainv_c32.release();
-            }
-            if (!getenv_flag("TSV_AS_COARSE_F64") && !getenv_flag("TSV_AS_COARSE_DENSE")) {
-                as2.sym_nt = static_cast<int>((Ncs + kSymT - 1) / kSymT);
-                const long long ntiles = static_cast<long long>(as2.sym_nt) * (as2.sym_nt + 1) / 2;
-                const long long tot = ntiles * kSymT * kSymT;
-                as2.sym_tiles.alloc(static_cast<size_t>(tot));
-                as2.sym_part.alloc(static_cast<size_t>(as2.sym_nt) * as2.sym_nt * kSymT);
-                as2.dotpart.alloc(static_cast<size_t>(as2.sym_nt));
-                as_pack_sym_tiles_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, stream>>>(
-                    as2.ainv_c.ptr, as2.Nc, as2.sym_tiles.ptr, tot);
-            } else {
-                as2.sym_nt = 0;
-                as2.sym_tiles.release();
-                as2.sym_part.release();
-            }
-            CK(cudaGetLastError());
+        as2.kcell_d.upload(kcell.data(), kcell.size(), stream);
+        if (!coarse_f64 && coarse_dense) {
+            as2.ldc32 = static_cast<int>(round_up(Ncs, 32));
+            as2.ainv_c32.alloc(Ncs * as2.ldc32);
+        } else {
+            as2.ainv_c32.release();
         }
+        long long sym_total = 0;
+        if (!coarse_f64 && !coarse_dense) {
+            as2.sym_nt = static_cast<int>((Ncs + kSymT - 1) / kSymT);
+            sym_total = static_cast<long long>(as2.sym_nt) * (as2.sym_nt + 1) / 2 * kSymT * kSymT;
+            as2.sym_tiles.alloc(static_cast<size_t>(sym_total));
+            as2.sym_part.alloc(static_cast<size_t>(as2.sym_nt) * as2.sym_nt * kSymT);
+            as2.dotpart.alloc(static_cast<size_t>(as2.sym_nt));
+        } else {
+            as2.sym_nt = 0;
+            as2.sym_tiles.release();
+            as2.sym_part.release();
+        }
+        if (!solver2.sol && (cusolverDnCreate(&solver2.sol) != CUSOLVER_STATUS_SUCCESS ||
+                             cublasCreate(&solver2.blas) != CUBLAS_STATUS_SUCCESS))
+            throw StatusError(TSV_ECUDA, "schwarz2: cuSOLVER/cuBLAS init failed");
+        cusolverDnSetStream(solver2.sol, side);
+        {
+            int lw1 = 0, lw2 = 0;
+            if (cusolverDnDpotrf_bufferSize(solver2.sol, CUBLAS_FILL_MODE_LOWER, as2.Nc, as2.ainv_c.ptr, as2.Nc, &lw1) !=
+                    CUSOLVER_STATUS_SUCCESS ||
+                cusolverDnDpotri_bufferSize(solver2.sol, CUBLAS_FILL_MODE_LOWER, as2.Nc, as2.ainv_c.ptr, as2.Nc, &lw2) !=
+                    CUSOLVER_STATUS_SUCCESS)
+                throw StatusError(TSV_ECUDA, "schwarz2: cuSOLVER buffer query failed");
+            as2.cwork.alloc(static_cast<size_t>(std::max(std::max(lw1, lw2), 1)));
+        }
+        CK(cudaEventRecord(ev_fork, stream));
+        CK(cudaStreamWaitEvent(side, ev_fork, 0));
+        std::exception_ptr coarse_err;
+        std::thread coarse_worker([&, Ncs, sym_total] {
+            try {
+                cudaSetDevice(device);
+                const cudaStream_t cs = side;
+                for (int py = 0; py < 2; ++py)
+                    for (int px = 0; px < 2; ++px) {
+                        const long long cnt = static_cast<long long>((as2.SX - px + 1) / 2) * ((as2.SY - py + 1) / 2) * 576;
+                        if (cnt <= 0) continue;
+                        as_coarse_scatter_kernel<<<static_cast<unsigned>((cnt + 255) / 256), 256, 0, cs>>>(
+                            as2.kcell_d.ptr, as2.SX, as2.SY, px, py, as2.ainv_c.ptr, as2.Nc);
+                    }
+                as_fix_zero_rows_kernel<<<static_cast<unsigned>((Ncs + 7) / 8), 256, 0, cs>>>(as2.ainv_c.ptr, as2.Nc);
+                spd_inverse_inplace(solver2, as2.ainv_c.ptr, as2.Nc, as2.cwork, cinfo.ptr);
+                as_symmetrize_kernel<<<static_cast<unsigned>((Ncs * Ncs + 255) / 256), 256, 0, cs>>>(as2.ainv_c.ptr,
+                                                                                                   as2.Nc);
+                if (as2.ainv_c32.ptr) {
+                    const size_t tot = Ncs * as2.ldc32;
+                    as_coarse_to_f32_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, cs>>>(
+                        as2.ainv_c.ptr, as2.Nc, as2.ldc32, as2.ainv_c32.ptr);
+                }
+                if (as2.sym_nt)
+                    as_pack_sym_tiles_kernel<<<static_cast<unsigned>((sym_total + 255) / 256), 256, 0, cs>>>(
+                        as2.ainv_c.ptr, as2.Nc, as2.sym_tiles.ptr, sym_total);
+                CK(cudaGetLastError());
+            } catch (...) {
+                coarse_err = std::current_exception();
+            }
+        });
+        struct Joiner {
+            std::thread &t;
+            ~Joiner() {
+                if (t.joinable()) t.join();
+            }
+        } joiner{coarse_worker};
         tick("coarse inverse (enqueued)");
         // --- 2. neighbourhood types: own kind, the 4 edge neighbours' kinds
         // (or absence), corner neighbours' presence, constrained pattern.
@@ -1008,6 +1059,11 @@ struct tsv_ctx {
         }
         as2.z.alloc(N);
         tick("panel tables");
+        coarse_worker.join();
+        if (coarse_err) std::rethrow_exception(coarse_err);
+        CK(cudaEventRecord(ev_join, side));
+        CK(cudaStreamWaitEvent(stream, ev_join, 0));
+        tick("coarse inverse joined");
         {
             std::vector<int> hinfo(infos.count), hc(2);
             d2h(hinfo.data(), infos.ptr, hinfo.size() * sizeof(int), stream);

@@ -1,6 +1,8 @@
 #include "host_index.hpp"
 
 #include <algorithm>
+#include <thread>
+#include <vector>
 
 namespace tsvb200 {
 
@@ -60,6 +62,13 @@ GlobalIndex index_global_nodes(const ArrayLayout& layout, const NodeLayout& node
     const std::size_t slots = static_cast<std::size_t>(idx.lat_x) * idx.lat_y * idx.lat_z;
     if (slots >= 0x7fffffffULL) throw Error("index_global_nodes: lattice too large for 32-bit node ids");
     idx.node_of_lattice.assign(slots, -1);
+    {
+        // node count: every lattice point on an x- or y-face plane, plus the
+        // interior points of the bottom/top planes
+        const std::size_t fx = layout.cols + 1, fy = layout.rows + 1;
+        const std::size_t on_xy = fx * idx.lat_y + fy * idx.lat_x - fx * fy;
+        idx.lattice_of_node.reserve(on_xy * idx.lat_z + 2 * (static_cast<std::size_t>(idx.lat_x) * idx.lat_y - on_xy));
+    }
     // A lattice point is skipped only when it is off every block face plane
     // in x and in y and off the top/bottom planes.
     for (std::uint32_t gz = 0; gz < idx.lat_z; ++gz) {
@@ -83,11 +92,22 @@ std::vector<std::uint32_t> dof_map(const ArrayLayout& layout, const GlobalIndex&
                                    const NodeLayout& node_layout) {
     const std::size_t n = node_layout.reduced_dofs();
     std::vector<std::uint32_t> out(layout.cell_count() * n);
-    for (std::uint32_t r = 0; r < layout.rows; ++r)
-        for (std::uint32_t c = 0; c < layout.cols; ++c) {
-            const std::size_t b = static_cast<std::size_t>(r) * layout.cols + c;
-            for (std::size_t a = 0; a < n; ++a) out[b * n + a] = index.global_dof(r, c, node_layout, a);
-        }
+    // rows are independent: split them over the host threads (same values)
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), layout.rows));
+    auto work = [&](unsigned w) {
+        for (std::uint32_t r = w; r < layout.rows; r += nt)
+            for (std::uint32_t c = 0; c < layout.cols; ++c) {
+                const std::size_t b = static_cast<std::size_t>(r) * layout.cols + c;
+                for (std::size_t a = 0; a < n; ++a) out[b * n + a] = index.global_dof(r, c, node_layout, a);
+            }
+    };
+    if (nt == 1 || layout.cell_count() * n < (1u << 16)) {
+        for (unsigned w = 0; w < nt; ++w) work(w);
+        return out;
+    }
+    std::vector<std::thread> pool;
+    for (unsigned w = 0; w < nt; ++w) pool.emplace_back(work, w);
+    for (auto& t : pool) t.join();
     return out;
 }
 

@@ -13,7 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 3 --no-jacobi-leg --no-cpu-baseline --e2e-steps 0 > $out/ncu_bench.log 2>&1
 echo "ncu exit $?" >> $out/ncu_bench.log
 # full ncu captures of the dominant kernels (K1 operator apply, K7 stress)
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_nt_f64 --launch-skip 12 -c 1 \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_nt_f64 --launch-skip 3 -c 1 \
   -o $out/k1_full python tools/prof_as.py 3 > $out/ncu_k1.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:stress_kernel -c 1 \
   -o $out/k7_full python tools/prof_recover.py 3 > $out/ncu_k7.log 2>&1
