@@ -160,6 +160,17 @@ struct RomHost {
     size_t n = 0, n_fine = 0, cells[3] = {0, 0, 0};
     uint8_t fingerprint[32] = {};
     DevBuf<double> d_k, d_phi, d_ut, d_hinv, d_grid[3], d_bel;
+    // K6 split: d_phi / d_ut hold the dense basis rows only (n_dense, in fine
+    // DoF order, d_dmap = their fine DoFs); the sparse (surface) rows are CSR
+    size_t n_dense = 0, n_sparse = 0;
+    DevBuf<int> d_dmap, d_sp_ptr, d_sp_dof, d_sp_col;
+    DevBuf<double> d_sp_val, d_ut_full;
+    // surface rows grouped by (face, component): small dense GEMMs (k6_face_kernel)
+    int n_groups = 0, max_group_rows = 0, max_group_k = 0;
+    DevBuf<int4> d_ginfo;
+    DevBuf<int> d_gcol, d_gdof;
+    DevBuf<double> d_gwt;
+    DevBuf<long long> d_gwoff;
     DevBuf<uint8_t> d_em;
     // Ozaki digit planes of K_r (int8 K1): [S][rows][KA], row exponents
     int oz_s = 0;
@@ -1576,6 +1587,77 @@ struct tsv_ctx {
         return m.cells[0] * m.cells[1] * m.cells[2];
     }
 
+    // K6: U rows of GEMM tiles [t, t1) (U row = GEMM row - t kBM) =
+    // Q Phi^T + dT u_T^T: the dense basis rows on the DMMA GEMM (scattered to
+    // their fine DoFs through d_dmap), the sparse surface rows on k6_sparse_kernel.
+    void launch_k6(const RomHost &mk, size_t t, size_t t1, double *Uout, size_t ldu) {
+        GemmParams gp{};
+        gp.A = X.ptr + t * kBM * ldk;
+        gp.lda = static_cast<long long>(ldk);
+        gp.Bt[0] = gp.Bt[1] = mk.d_phi.ptr;
+        gp.ldb = static_cast<long long>(ldk);
+        gp.tile_kind = nullptr;
+        gp.C = Uout;
+        gp.ldc = static_cast<long long>(ldu);
+        gp.m_tiles = static_cast<int>(t1 - t);
+        gp.n_tiles = static_cast<int>(round_up(std::max<size_t>(mk.n_dense, 1), kBN) / kBN);
+        gp.k_chunks = static_cast<int>(ldk / kKC);
+        gp.n_valid = static_cast<int>(mk.n_dense);
+        gp.n_store = static_cast<int>(mk.n_dense);
+        gp.row_scale = row_dt_d.ptr + t * kBM;
+        gp.col_bias[0] = gp.col_bias[1] = mk.d_ut.ptr;
+        gp.done = nullptr;
+        gp.tile_counter = tile_counter.ptr;
+        gp.n_major = 1;
+        gp.col_map = mk.n_dense < mk.n_fine ? mk.d_dmap.ptr : nullptr;
+        if (mk.n_dense) {
+            gemm_nt_f64<K6Cfg><<<k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
+            ++launches;
+        }
+        if (mk.n_groups) {
+            K6Face fp{};
+            fp.X = X.ptr + t * kBM * ldk;
+            fp.ldk = static_cast<long long>(ldk);
+            fp.rows = static_cast<int>((t1 - t) * kBM);
+            fp.row_dt = row_dt_d.ptr + t * kBM;
+            fp.ginfo = mk.d_ginfo.ptr;
+            fp.gcol = mk.d_gcol.ptr;
+            fp.gwt = mk.d_gwt.ptr;
+            fp.gwoff = mk.d_gwoff.ptr;
+            fp.gdof = mk.d_gdof.ptr;
+            fp.ut = mk.d_ut_full.ptr;
+            fp.U = Uout;
+            fp.ldu = static_cast<long long>(ldu);
+            dim3 grid(static_cast<unsigned>((fp.rows + 32 * kFaceSub - 1) / (32 * kFaceSub)), static_cast<unsigned>(mk.n_groups),
+                      static_cast<unsigned>((mk.max_group_rows + 127) / 128));
+            const size_t smem = static_cast<size_t>(mk.max_group_k) * (32 + 128) * sizeof(double);
+            CK(cudaFuncSetAttribute(k6_face_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            k6_face_kernel<<<grid, 256, smem, stream>>>(fp);
+            ++launches;
+        }
+        if (mk.n_sparse) {
+            K6Sparse sp{};
+            sp.X = X.ptr + t * kBM * ldk;
+            sp.ldk = static_cast<long long>(ldk);
+            sp.rows = static_cast<int>((t1 - t) * kBM);
+            sp.row_dt = row_dt_d.ptr + t * kBM;
+            sp.n_sparse = static_cast<int>(mk.n_sparse);
+            sp.ptr = mk.d_sp_ptr.ptr;
+            sp.dof = mk.d_sp_dof.ptr;
+            sp.col = mk.d_sp_col.ptr;
+            sp.val = mk.d_sp_val.ptr;
+            sp.ut = mk.d_ut_full.ptr;
+            sp.U = Uout;
+            sp.ldu = static_cast<long long>(ldu);
+            const size_t smem = static_cast<size_t>(kK6sRows) * ldk * sizeof(double);
+            CK(cudaFuncSetAttribute(k6_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            dim3 grid(static_cast<unsigned>((sp.rows + kK6sRows - 1) / kK6sRows), 1);
+            k6_sparse_kernel<<<grid, 256, smem, stream>>>(sp);
+            ++launches;
+        }
+        CK(cudaGetLastError());
+    }
+
     // Recover cells [c0, c1) into device buffer `out` (cells-relative).
     // Recover cells [c0, c1) into device buffer `out` (cells-relative):
     // points = 8 / 1 -> stress_kernel; points = -res -> cut-plane samples.
@@ -1621,25 +1703,7 @@ struct tsv_ctx {
             while (t1 < m_tiles && need[t1] && t1 - t < chunk_tiles && tile_kind[t1] == tile_kind[t]) ++t1;
             const int kind = tile_kind[t];
             const RomHost &mk = rom[kind];
-            GemmParams gp{};
-            gp.A = X.ptr + t * kBM * ldk;
-            gp.lda = static_cast<long long>(ldk);
-            gp.Bt[0] = gp.Bt[1] = mk.d_phi.ptr;
-            gp.ldb = static_cast<long long>(ldk);
-            gp.tile_kind = nullptr;
-            gp.C = U.ptr;
-            gp.ldc = static_cast<long long>(ldu);
-            gp.m_tiles = static_cast<int>(t1 - t);
-            gp.n_tiles = static_cast<int>(round_up(mk.n_fine, kBN) / kBN);
-            gp.k_chunks = static_cast<int>(ldk / kKC);
-            gp.n_valid = static_cast<int>(mk.n_fine);
-            gp.n_store = static_cast<int>(mk.n_fine);
-            gp.row_scale = row_dt_d.ptr + t * kBM;
-            gp.col_bias[0] = gp.col_bias[1] = mk.d_ut.ptr;
-            gp.done = nullptr;
-            gp.tile_counter = tile_counter.ptr;
-            gp.n_major = 1;
-            gemm_nt_f64<K6Cfg><<<k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
+            launch_k6(mk, t, t1, U.ptr, ldu);
             if (points > 0) {
                 sp.U = U.ptr;
                 sp.j0 = static_cast<int>(t * kBM);
@@ -1672,7 +1736,7 @@ struct tsv_ctx {
                 dim3 grid(static_cast<unsigned>((t1 - t) * kBM), static_cast<unsigned>((res * res + 255) / 256));
                 cutplane_kernel<<<grid, 256, 0, stream>>>(cp);
             }
-            launches += 2;
+            ++launches;  // stress or cut plane (launch_k6 counts its own)
             CK(cudaGetLastError());
             t = t1;
         }
@@ -1919,15 +1983,103 @@ int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
             m.oz_s = 0;  // int8 digit planes are rebuilt on next use
         }
         {
-            const size_t rows = round_up(n_fine, kBN);
-            std::vector<double> pp(rows * ldk, 0.0);
+            // Basis rows with at most n/4 non-zeros (surface nodes: q^2, q or 1
+            // interpolation weights) go to the CSR path (k6_sparse_kernel), the
+            // rest to the dense GEMM.
+            const size_t kSparseRowMax = n / 4;
+            const bool split = !tsv_ctx::getenv_flag("TSV_K6_DENSE");
             const size_t nn = n / 3;
-            for (size_t f = 0; f < n_fine; ++f)
-                for (size_t a = 0; a < n; ++a) pp[f * ldk + pidx(a, nn)] = d->basis[f * n + a];
+            std::vector<int> dmap, sp_ptr(1, 0), sp_dof, sp_col;
+            std::vector<double> sp_val;
+            // (face, component) groups of the surface rows; a row whose group's
+            // column union exceeds kFaceK stays on the CSR path
+            const size_t nx = m.cells[0] + 1, ny = m.cells[1] + 1;
+            std::vector<std::vector<int>> grows(18);
+            std::vector<std::vector<char>> gmask(18, std::vector<char>(n, 0));
+            std::vector<int> sparse_rows;
+            for (size_t f = 0; f < n_fine; ++f) {
+                const double *row = d->basis + f * n;
+                size_t nz = 0;
+                for (size_t a = 0; a < n; ++a) nz += row[a] != 0.0;
+                if (!(split && nz <= kSparseRowMax)) {
+                    dmap.push_back(static_cast<int>(f));
+                    continue;
+                }
+                const size_t node = f / 3, comp = f % 3;
+                const size_t i = node % nx, j = (node / nx) % ny, k = node / (nx * ny);
+                const int face = k == 0 ? 0 : k == m.cells[2] ? 1 : j == 0 ? 2 : j == m.cells[1] ? 3 : i == 0 ? 4 : i == m.cells[0] ? 5 : -1;
+                if (face < 0 || tsv_ctx::getenv_flag("TSV_K6_CSR")) {
+                    sparse_rows.push_back(static_cast<int>(f));
+                    continue;
+                }
+                grows[face * 3 + comp].push_back(static_cast<int>(f));
+                for (size_t a = 0; a < n; ++a)
+                    if (row[a] != 0.0) gmask[face * 3 + comp][a] = 1;
+            }
+            std::vector<int4> ginfo;
+            std::vector<int> gcol, gdof;
+            std::vector<double> gwt;
+            std::vector<long long> gwoff;
+            m.max_group_rows = 0;
+            m.max_group_k = 0;
+            for (int g = 0; g < 18; ++g) {
+                if (grows[g].empty()) continue;
+                std::vector<int> cols;  // reduced DoFs a (reference order)
+                for (size_t a = 0; a < n; ++a)
+                    if (gmask[g][a]) cols.push_back(static_cast<int>(a));
+                if (cols.size() > static_cast<size_t>(kFaceK)) {
+                    sparse_rows.insert(sparse_rows.end(), grows[g].begin(), grows[g].end());
+                    continue;
+                }
+                const int nr = static_cast<int>(grows[g].size()), K = static_cast<int>(cols.size());
+                ginfo.push_back(make_int4(static_cast<int>(gdof.size()), nr, static_cast<int>(gcol.size()), K));
+                gwoff.push_back(static_cast<long long>(gwt.size()));
+                for (int a : cols) gcol.push_back(static_cast<int>(pidx(static_cast<size_t>(a), nn)));
+                gdof.insert(gdof.end(), grows[g].begin(), grows[g].end());
+                for (int kk = 0; kk < K; ++kk)  // W^T [K][rows]
+                    for (int r = 0; r < nr; ++r) gwt.push_back(d->basis[static_cast<size_t>(grows[g][r]) * n + cols[kk]]);
+                m.max_group_rows = std::max(m.max_group_rows, nr);
+                m.max_group_k = std::max(m.max_group_k, K);
+            }
+            m.n_groups = static_cast<int>(ginfo.size());
+            std::sort(sparse_rows.begin(), sparse_rows.end());
+            for (int f : sparse_rows) {
+                const double *row = d->basis + static_cast<size_t>(f) * n;
+                sp_dof.push_back(f);
+                for (size_t a = 0; a < n; ++a)
+                    if (row[a] != 0.0) {
+                        sp_col.push_back(static_cast<int>(pidx(a, nn)));
+                        sp_val.push_back(row[a]);
+                    }
+                sp_ptr.push_back(static_cast<int>(sp_col.size()));
+            }
+            if (m.n_groups) {
+                m.d_ginfo.upload(ginfo.data(), ginfo.size(), ctx->stream);
+                m.d_gcol.upload(gcol.data(), gcol.size(), ctx->stream);
+                m.d_gdof.upload(gdof.data(), gdof.size(), ctx->stream);
+                m.d_gwt.upload(gwt.data(), gwt.size(), ctx->stream);
+                m.d_gwoff.upload(gwoff.data(), gwoff.size(), ctx->stream);
+            }
+            m.n_dense = dmap.size();
+            m.n_sparse = sp_dof.size();
+            const size_t rows = round_up(std::max<size_t>(m.n_dense, 1), kBN);
+            std::vector<double> pp(rows * ldk, 0.0), ut(rows, 0.0);
+            for (size_t i = 0; i < m.n_dense; ++i) {
+                const size_t f = static_cast<size_t>(dmap[i]);
+                for (size_t a = 0; a < n; ++a) pp[i * ldk + pidx(a, nn)] = d->basis[f * n + a];
+                ut[i] = d->thermal[f];
+            }
             m.d_phi.upload(pp.data(), pp.size(), ctx->stream);
-            std::vector<double> ut(rows, 0.0);
-            std::memcpy(ut.data(), d->thermal, n_fine * sizeof(double));
             m.d_ut.upload(ut.data(), ut.size(), ctx->stream);
+            m.d_ut_full.upload(d->thermal, n_fine, ctx->stream);
+            if (m.n_dense < n_fine) m.d_dmap.upload(dmap.data(), dmap.size(), ctx->stream);
+            if (m.n_sparse) {
+                m.d_sp_ptr.upload(sp_ptr.data(), sp_ptr.size(), ctx->stream);
+                m.d_sp_dof.upload(sp_dof.data(), sp_dof.size(), ctx->stream);
+                m.d_sp_col.upload(sp_col.data(), std::max<size_t>(sp_col.size(), 1), ctx->stream);
+                m.d_sp_val.upload(sp_val.data(), std::max<size_t>(sp_val.size(), 1), ctx->stream);
+            }
+            if (m.n_dense == n_fine) m.d_dmap.release();
             CK(cudaStreamSynchronize(ctx->stream));
         }
         std::vector<double> hinv;
@@ -2259,23 +2411,7 @@ int tsv_block_field(tsv_ctx *ctx, uint64_t cell, double *out) {
         const size_t ldu = round_up(mk.n_fine, 8);
         ctx->launch_scatter(ctx->x.ptr, 1);
         ctx->U.alloc(std::max(ctx->U.count, kBM * ldu));
-        GemmParams gp{};
-        gp.A = ctx->X.ptr + t * kBM * ctx->ldk;
-        gp.lda = static_cast<long long>(ctx->ldk);
-        gp.Bt[0] = gp.Bt[1] = mk.d_phi.ptr;
-        gp.ldb = static_cast<long long>(ctx->ldk);
-        gp.C = ctx->U.ptr;
-        gp.ldc = static_cast<long long>(ldu);
-        gp.m_tiles = 1;
-        gp.n_tiles = static_cast<int>(round_up(mk.n_fine, kBN) / kBN);
-        gp.k_chunks = static_cast<int>(ctx->ldk / kKC);
-        gp.n_valid = gp.n_store = static_cast<int>(mk.n_fine);
-        gp.row_scale = ctx->row_dt_d.ptr + t * kBM;
-        gp.col_bias[0] = gp.col_bias[1] = mk.d_ut.ptr;
-        gp.tile_counter = ctx->tile_counter.ptr;
-        gemm_nt_f64<K6Cfg><<<ctx->k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, ctx->stream>>>(gp);
-        ++ctx->launches;
-        CK(cudaGetLastError());
+        ctx->launch_k6(mk, t, t + 1, ctx->U.ptr, ldu);
         CK(cudaMemcpyAsync(out, ctx->U.ptr + (j - t * kBM) * ldu, mk.n_fine * sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));

@@ -41,6 +41,7 @@ struct GemmParams {
     unsigned *tile_counter;      // [2] {next tile, exited CTAs}, zero between launches
     int n_major;                 // tile order: 0 = M major (K1: A streamed once, K_r in L2),
                                  // 1 = N major (K6: Phi streamed once, the Q chunk in L2)
+    const int *col_map;          // nullable: output column of GEMM column (K6: dense fine DoF rows)
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
@@ -186,6 +187,12 @@ __device__ __forceinline__ void gemm_epilogue(const GemmParams &p, int mt, int n
                 const double s = p.row_scale[row];
                 v0 += s * b0;
                 v1 += s * b1;
+            }
+            if (p.col_map) {
+                double *rowp = p.C + row * p.ldc;
+                rowp[p.col_map[col]] = v0;
+                if (col + 1 < p.n_store) rowp[p.col_map[col + 1]] = v1;
+                continue;
             }
             double *dst = p.C + row * p.ldc + col;
             if (col + 1 < p.n_store) {
@@ -704,6 +711,147 @@ __global__ void gather_vec_kernel(int n_nodes, int nn, const int *slots, const u
             y[dof] = cmask[dof] ? x[dof] : acc;
         } else {
             y[dof] = cmask[dof] ? x[dof] : y[dof] - acc;
+        }
+    }
+}
+
+// K6s: the fine DoFs whose basis rows are sparse (the block's surface nodes,
+// pinned to the Lagrange interpolation of one face, edge or corner: <= q^2
+// non-zeros of n) are reconstructed from a CSR copy of those rows instead of
+// the dense GEMM: u[dof] = sum_e Phi[dof][col_e] q[col_e] + dT u_T[dof]
+// (reconstruct_block_field, global_stage.cpp:215-230, without the exact zeros).
+// A CTA takes kK6sRows block rows, staged in shared memory column-major
+// (xs[col][row]: one entry's kK6sRows operands are 64 contiguous bytes), and
+// one of gridDim.y slices of the sparse DoFs; each CSR entry is read once per
+// kK6sRows rows.
+constexpr int kK6sRows = 8;
+struct K6Sparse {
+    const double *X;        // Q panel rows of the chunk (row stride ldk)
+    long long ldk;
+    int rows;               // rows in the chunk
+    const double *row_dt;   // dT per chunk row
+    int n_sparse;
+    const int *ptr, *dof, *col;
+    const double *val, *ut;  // ut: u_T over all fine DoFs
+    double *U;
+    long long ldu;
+};
+
+__global__ void __launch_bounds__(256) k6_sparse_kernel(K6Sparse p) {
+    extern __shared__ double xs[];  // [ldk][kK6sRows]
+    const int r0 = blockIdx.x * kK6sRows;
+    const int nr = min(kK6sRows, p.rows - r0);
+    for (int i = threadIdx.x; i < kK6sRows * p.ldk; i += blockDim.x) {
+        const int r = static_cast<int>(i / p.ldk), c = static_cast<int>(i % p.ldk);
+        xs[c * kK6sRows + r] = r < nr ? p.X[(static_cast<long long>(r0) + r) * p.ldk + c] : 0.0;
+    }
+    __syncthreads();
+    double dt[kK6sRows];
+#pragma unroll
+    for (int r = 0; r < kK6sRows; ++r) dt[r] = r < nr ? p.row_dt[r0 + r] : 0.0;
+    const int per = (p.n_sparse + gridDim.y - 1) / gridDim.y;
+    const int j0 = blockIdx.y * per, j1 = min(p.n_sparse, j0 + per);
+    for (int j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        double acc[kK6sRows];
+#pragma unroll
+        for (int r = 0; r < kK6sRows; ++r) acc[r] = 0.0;
+        const int e1 = p.ptr[j + 1];
+        for (int e = p.ptr[j]; e < e1; ++e) {
+            const int c = __ldg(p.col + e);
+            const double v = __ldg(p.val + e);
+            const double2 *xc = reinterpret_cast<const double2 *>(xs + c * kK6sRows);
+#pragma unroll
+            for (int h = 0; h < kK6sRows / 2; ++h) {
+                const double2 x2 = xc[h];
+                acc[2 * h] += v * x2.x;
+                acc[2 * h + 1] += v * x2.y;
+            }
+        }
+        const int dof = p.dof[j];
+        const double ut = p.ut[dof];
+#pragma unroll
+        for (int r = 0; r < kK6sRows; ++r)
+            if (r < nr) p.U[(static_cast<long long>(r0) + r) * p.ldu + dof] = acc[r] + dt[r] * ut;
+    }
+}
+
+// K6f: the surface rows of Phi grouped by (face, component): every row of a
+// group interpolates from the same <= kFaceK reduced DoFs (the face's
+// interface nodes, one component), so a group is a small dense GEMM
+// U[rows][dof_g] = Q[rows][cols_g] W_g^T + dT u_T. A CTA computes 32 block
+// rows x 128 group rows (4 x 4 per thread) with K <= kFaceK staged k-major.
+constexpr int kFaceK = 64;
+struct K6Face {
+    const double *X;          // Q panel rows of the chunk (row stride ldk)
+    long long ldk;
+    int rows;                 // rows in the chunk
+    const double *row_dt;     // dT per chunk row
+    const int4 *ginfo;        // per group: {row offset, rows, col offset, K}
+    const int *gcol;          // [sum K] panel columns
+    const double *gwt;        // per group: W^T [K][rows] at K-offset * ... (wt_off)
+    const long long *gwoff;   // per group: offset of its W^T in gwt
+    const int *gdof;          // [sum rows] fine DoF of each group row
+    const double *ut;         // u_T over all fine DoFs
+    double *U;
+    long long ldu;
+};
+
+constexpr int kFaceSub = 8;  // 32-row sub-tiles per CTA (the W tile is staged once)
+__global__ void __launch_bounds__(256) k6_face_kernel(K6Face p) {
+    extern __shared__ __align__(16) double k6f_smem[];  // ws [K][128], then qs [K][32]
+    const int4 gi4 = p.ginfo[blockIdx.y];
+    const int row_off = gi4.x, nrows = gi4.y, col_off = gi4.z, K = gi4.w;
+    double (*ws)[128] = reinterpret_cast<double (*)[128]>(k6f_smem);
+    double (*qs)[32] = reinterpret_cast<double (*)[32]>(k6f_smem + static_cast<size_t>(K) * 128);
+    const int t0 = blockIdx.z * 128;
+    if (t0 >= nrows) return;
+    const int tid = threadIdx.x;
+    const double *wt = p.gwt + p.gwoff[blockIdx.y];
+    for (int i = tid; i < K * 128; i += 256) {
+        const int k = i >> 7, j = i & 127;
+        ws[k][j] = t0 + j < nrows ? wt[static_cast<long long>(k) * nrows + t0 + j] : 0.0;
+    }
+    const int gq = tid & 31, bq = tid >> 5;  // group rows gq + 32 b (coalesced stores), block rows 4 bq + a
+    int dof[4];
+    double ut[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int j = t0 + gq + 32 * b;
+        dof[b] = j < nrows ? p.gdof[row_off + j] : -1;
+        ut[b] = j < nrows ? p.ut[dof[b]] : 0.0;
+    }
+    for (int sub = 0; sub < kFaceSub; ++sub) {
+        const int r0 = (blockIdx.x * kFaceSub + sub) * 32;
+        if (r0 >= p.rows) break;
+        __syncthreads();  // ws staged / previous sub-tile's qs consumed
+        for (int i = tid; i < K * 32; i += 256) {
+            const int k = i >> 5, r = i & 31;
+            qs[k][r] = r0 + r < p.rows ? p.X[(static_cast<long long>(r0) + r) * p.ldk + p.gcol[col_off + k]] : 0.0;
+        }
+        __syncthreads();
+        double acc[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int k = 0; k < K; ++k) {
+            const double2 q01 = *reinterpret_cast<const double2 *>(&qs[k][bq * 4]);
+            const double2 q23 = *reinterpret_cast<const double2 *>(&qs[k][bq * 4 + 2]);
+            const double q[4] = {q01.x, q01.y, q23.x, q23.y};
+            const double w[4] = {ws[k][gq], ws[k][gq + 32], ws[k][gq + 64], ws[k][gq + 96]};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] += q[a] * w[b];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int r = r0 + bq * 4 + a;
+            if (r >= p.rows) continue;
+            const double dt = p.row_dt[r];
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (dof[b] >= 0) p.U[static_cast<long long>(r) * p.ldu + dof[b]] = acc[a][b] + dt * ut[b];
         }
     }
 }
