@@ -227,6 +227,11 @@ int tsv_build_rom(int device, const tsv_local_desc *desc, tsv_rom_out *out, char
  * PCIe/C2C rate (cudaHostRegister); unregister before freeing it. */
 int tsv_host_register(void *ptr, size_t bytes);
 int tsv_host_unregister(void *ptr);
+/* Allocate / free page-locked host memory for results (cudaHostAlloc):
+ * device-to-host copies into it run ~10% faster than into registered
+ * pageable memory on this platform (57 vs 51 GB/s). */
+int tsv_host_alloc(size_t bytes, void **ptr);
+int tsv_host_free(void *ptr);
 
 /* FP64 roofline denominators measured live on `device`: register-only
  * DMMA.8x8x4 (mma.sync f64) and DFMA issue loops over all SMs. */

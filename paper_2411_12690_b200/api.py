@@ -331,6 +331,35 @@ class GpuGlobalStage:
         return t
 
 
+class PinnedArray:
+    """A numpy array in page-locked host memory (tsv_host_alloc / cudaHostAlloc):
+    the destination for tsv_recover / tsv_copy_stress at full PCIe rate.
+    `.array` is the view; `close()` (or garbage collection) frees it."""
+
+    def __init__(self, shape, dtype=np.float64):
+        self._L = native.load()
+        self.dtype = np.dtype(dtype)
+        n = int(np.prod(shape)) * self.dtype.itemsize
+        self._ptr = C.c_void_p()
+        rc = self._L.tsv_host_alloc(max(n, 1), C.byref(self._ptr))
+        if rc != 0:
+            raise Error(f"tsv_host_alloc({n} bytes) failed ({rc})")
+        buf = (C.c_char * max(n, 1)).from_address(self._ptr.value)
+        self.array = np.frombuffer(buf, dtype=self.dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def close(self):
+        if self._ptr is not None and self._ptr.value:
+            self.array = None
+            self._L.tsv_host_free(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def build_rom(q, geometry, grid, materials, kind: int = 0, device: int = 0) -> ReducedOrderModel:
     """One-shot local stage on the GPU (rom::build_rom, rom.cpp:134-253):
     the ROM of one unit block. Input of the online stage; timed separately

@@ -1784,6 +1784,15 @@ int tsv_host_register(void *ptr, size_t bytes) {
 
 int tsv_host_unregister(void *ptr) { return cudaHostUnregister(ptr) == cudaSuccess ? TSV_OK : TSV_ECUDA; }
 
+int tsv_host_alloc(size_t bytes, void **ptr) {
+    if (!ptr) return TSV_EINVAL;
+    *ptr = nullptr;
+    const cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocDefault);
+    return e == cudaSuccess ? TSV_OK : (e == cudaErrorMemoryAllocation ? TSV_ENOMEM : TSV_ECUDA);
+}
+
+int tsv_host_free(void *ptr) { return cudaFreeHost(ptr) == cudaSuccess ? TSV_OK : TSV_ECUDA; }
+
 int tsv_fp64_peak(int device, double *dmma_tflops, double *dfma_tflops) {
     if (cudaSetDevice(device) != cudaSuccess) return TSV_ECUDA;
     int sms = 0;

@@ -19,7 +19,7 @@ EXPORTS = [
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
     "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_precond_apply", "tsv_precond_setup", "tsv_debug_coarse", "tsv_solve", "tsv_set_solution", "tsv_recover",
     "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
-    "tsv_rom_dims", "tsv_rom_fingerprint", "tsv_rom_file_info", "tsv_build_rom", "tsv_load_rom_file", "tsv_save_rom_file", "tsv_host_register", "tsv_host_unregister", "tsv_fp64_peak",
+    "tsv_rom_dims", "tsv_rom_fingerprint", "tsv_rom_file_info", "tsv_build_rom", "tsv_load_rom_file", "tsv_save_rom_file", "tsv_host_register", "tsv_host_unregister", "tsv_host_alloc", "tsv_host_free", "tsv_fp64_peak",
 ]
 
 
@@ -115,6 +115,8 @@ def load(path: str = LIB_PATH):
         "tsv_get_timing": (i, [vp, P(Timing)]),
         "tsv_host_register": (i, [vp, sz]),
         "tsv_host_unregister": (i, [vp]),
+        "tsv_host_alloc": (i, [sz, C.POINTER(vp)]),
+        "tsv_host_free": (i, [vp]),
         "tsv_fp64_peak": (i, [i, P(d), P(d)]),
         "tsv_load_rom_file": (i, [vp, i, C.c_char_p, P(i), C.c_char_p, sz]),
         "tsv_save_rom_file": (i, [P(RomDesc), i, C.c_char_p, C.c_char_p, sz]),
