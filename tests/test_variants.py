@@ -1,0 +1,87 @@
+"""The default B200 code paths against their simpler variants, on the same
+inputs (GPU):
+
+- K6 split (dense DMMA GEMM over the interior basis rows, (face, component)
+  GEMMs over the surface rows) vs one dense GEMM (TSV_K6_DENSE) and vs the
+  CSR surface path (TSV_K6_CSR): the same recovered stress to rounding;
+- the symmetric packed-tile coarse solve of the Schwarz preconditioner vs the
+  dense FP32 GEMV (TSV_AS_COARSE_DENSE) and the FP64 one (TSV_AS_COARSE_F64):
+  M r agrees to FP32 rounding, and the PCG converges to the same u;
+- the split z = z_l + P z_c (tsv_precond_apply returns the assembled z):
+  M is symmetric to TF32 rounding, r1.(M r2) = r2.(M r1).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel_l2, stress_errors
+from paper_2411_12690_b200 import configs
+from paper_2411_12690_b200.api import IterOptions
+
+pytestmark = pytest.mark.gpu
+
+
+def _mixed(refpy):
+    from test_gpu_parity import make_case
+    rng = np.random.default_rng(5)
+    kinds = (rng.random(20) < 0.3).astype(np.uint8)
+    return make_case(refpy, configs.get(0), 4, 5, kinds, -270.0 + 40.0 * rng.random(20))
+
+
+@pytest.mark.parametrize("variant", ["TSV_K6_DENSE", "TSV_K6_CSR"])
+def test_k6_split_matches_dense(oracle_libs, native_lib, monkeypatch, variant):
+    refpy, _ = oracle_libs
+    out = {}
+    for mode in ("default", variant):
+        monkeypatch.delenv("TSV_K6_DENSE", raising=False)
+        monkeypatch.delenv("TSV_K6_CSR", raising=False)
+        if mode != "default":
+            monkeypatch.setenv(mode, "1")
+        sess, g = _mixed(refpy)  # the split is decided when the ROM is set
+        sol = g.solve_global(IterOptions(1e-12, 10000, "diagonal"))
+        out[mode] = (sol.u, g.recover(8), g.block_field(7))
+        g.close()
+    u0, s0, f0 = out["default"]
+    u1, s1, f1 = out[variant]
+    assert np.array_equal(u0, u1)  # the solve does not depend on the recovery path
+    mx, l2 = stress_errors(s0, s1)
+    assert mx.max() <= 1e-12 and l2.max() <= 1e-12
+    assert rel_l2(f0, f1) <= 1e-13
+
+
+@pytest.mark.parametrize("variant", ["TSV_AS_COARSE_DENSE", "TSV_AS_COARSE_F64"])
+def test_symmetric_coarse_matches_dense(oracle_libs, native_lib, monkeypatch, variant):
+    refpy, _ = oracle_libs
+    r = np.random.default_rng(2)
+    res = {}
+    for mode in ("default", variant):
+        monkeypatch.delenv("TSV_AS_COARSE_DENSE", raising=False)
+        monkeypatch.delenv("TSV_AS_COARSE_F64", raising=False)
+        if mode != "default":
+            monkeypatch.setenv(mode, "1")
+        sess, g = _mixed(refpy)
+        n = g.index().dof_count
+        rv = r.standard_normal(n) if mode == "default" else res["default"][0]
+        z = g.precond_apply(rv)
+        sol = g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
+        res[mode] = (rv, z, sol.u)
+        g.close()
+    _, z0, u0 = res["default"]
+    _, z1, u1 = res[variant]
+    assert rel_l2(z0, z1) <= 1e-5  # FP32 inverse storage, different summation order
+    assert rel_l2(u0, u1) <= 1e-10
+
+
+def test_schwarz_preconditioner_is_symmetric(oracle_libs, native_lib):
+    refpy, _ = oracle_libs
+    sess, g = _mixed(refpy)
+    n = g.index().dof_count
+    rng = np.random.default_rng(9)
+    r1, r2 = rng.standard_normal(n), rng.standard_normal(n)
+    a = r1 @ g.precond_apply(r2)
+    b = r2 @ g.precond_apply(r1)
+    assert abs(a - b) <= 1e-3 * max(abs(a), abs(b))  # TF32 operands of the local solves
+    # positive definite on these samples
+    assert r1 @ g.precond_apply(r1) > 0 and r2 @ g.precond_apply(r2) > 0
+    g.close()
