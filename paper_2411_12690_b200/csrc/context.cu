@@ -441,7 +441,7 @@ struct tsv_ctx {
         partial.alloc(2 * std::max<size_t>(vec_blocks, 1));
         layout_set = true;
         bc_set = false;
-        set_bc_mask(std::vector<uint8_t>(N, 0), std::vector<double>(N, 0.0));
+        set_bc_mask(std::vector<uint8_t>(N, 0), {});
         bc_set = false;
         CK(cudaStreamSynchronize(s));
     }
@@ -506,13 +506,19 @@ struct tsv_ctx {
     }
 
     // ------------------------------------------------------------------ BC
-    void set_bc_mask(std::vector<uint8_t> mask, std::vector<double> vals) {
+    // mask: constrained DoFs (reference numbering); vals: the prescribed
+    // (dof, value) pairs, sorted (only the non-zero values matter for lifting).
+    void set_bc_mask(std::vector<uint8_t> mask, const std::vector<std::pair<uint32_t, double>> &vals) {
         PhaseTimer pt("set_bc_mask");
         constrained = std::move(mask);
-        g = std::move(vals);
         any_g = false;
-        for (size_t i = 0; i < N; ++i)
-            if (constrained[i] && g[i] != 0.0) any_g = true;
+        for (const auto &e : vals)
+            if (e.second != 0.0) any_g = true;
+        g.clear();
+        if (any_g) {
+            g.assign(N, 0.0);
+            for (const auto &e : vals) g[e.first] = e.second;
+        }
         std::vector<uint8_t> cm_int(N);
         for (size_t in = 0; in < nodes; ++in)
             for (int c = 0; c < 3; ++c) cm_int[c * nodes + in] = constrained[3 * node_glob_of_int[in] + c];
@@ -2122,16 +2128,14 @@ int tsv_set_dirichlet(tsv_ctx *ctx, size_t count, const uint32_t *dofs, const do
         DirichletSet set;
         for (size_t i = 0; i < count; ++i) set.set(dofs[i], values[i]);
         std::vector<uint8_t> mask(ctx->N, 0);
-        std::vector<double> vals(ctx->N, 0.0);
         for (const auto &e : set.entries()) {
             if (e.first >= ctx->N)
                 throw StatusError(TSV_EINVAL, "apply_dirichlet_lifting: dof " + std::to_string(e.first) + " out of range");
             mask[e.first] = 1;
-            vals[e.first] = e.second;
         }
         cudaSetDevice(ctx->device);
         ctx->drop_graph();
-        ctx->set_bc_mask(std::move(mask), std::move(vals));
+        ctx->set_bc_mask(std::move(mask), set.entries());
         return TSV_OK;
     });
 }
@@ -2140,16 +2144,15 @@ int tsv_set_bc(tsv_ctx *ctx, int bc_kind) {
     return guarded(ctx, [&] {
         if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "set_bc: no layout set");
         if (bc_kind < 0 || bc_kind > 3) throw StatusError(TSV_EINVAL, "set_bc: unknown boundary condition");
+        PhaseTimer pt("  reduced_dirichlet");
         DirichletSet set = reduced_dirichlet(static_cast<BcKind>(bc_kind), ctx->index);
+        pt.lap("  bc mask");
         std::vector<uint8_t> mask(ctx->N, 0);
-        std::vector<double> vals(ctx->N, 0.0);
-        for (const auto &e : set.entries()) {
-            mask[e.first] = 1;
-            vals[e.first] = e.second;
-        }
+        for (const auto &e : set.entries()) mask[e.first] = 1;
         cudaSetDevice(ctx->device);
         ctx->drop_graph();
-        ctx->set_bc_mask(std::move(mask), std::move(vals));
+        pt.lap("  set_bc_mask");
+        ctx->set_bc_mask(std::move(mask), set.entries());
         return TSV_OK;
     });
 }

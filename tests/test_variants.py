@@ -85,3 +85,26 @@ def test_schwarz_preconditioner_is_symmetric(oracle_libs, native_lib):
     # positive definite on these samples
     assert r1 @ g.precond_apply(r1) > 0 and r2 @ g.precond_apply(r2) > 0
     g.close()
+
+
+def test_nonzero_dirichlet_lifting_rigid_translation(oracle_libs, native_lib):
+    """Non-zero prescribed values (b_f -= A_fc g, b_c = g; fem.cpp:223-260):
+    lifting every constrained u_z of the 3-2-1 set by delta is a rigid
+    translation, so u = u_0 + delta e_z and the stress is unchanged."""
+    refpy, _ = oracle_libs
+    sess, g = _mixed(refpy)
+    u0 = g.solve_global(IterOptions(1e-12, 10000, "schwarz2")).u
+    s0 = g.recover(8)
+    mask = g.constrained().astype(bool)
+    dofs = np.nonzero(mask)[0].astype(np.uint32)
+    delta = 1e-7
+    vals = np.where(dofs % 3 == 2, delta, 0.0)
+    g.set_dirichlet(dofs, vals)
+    u1 = g.solve_global(IterOptions(1e-12, 10000, "schwarz2")).u
+    shift = np.zeros_like(u0)
+    shift[2::3] = delta
+    assert rel_l2(u1, u0 + shift) <= 1e-9
+    assert np.abs(u1[dofs] - vals).max() <= 1e-10 * np.abs(u1).max()  # u_c = g
+    mx, _ = stress_errors(g.recover(8), s0)
+    assert mx.max() <= 1e-7
+    g.close()
