@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <utility>
 #include <exception>
 #include <vector>
 
@@ -687,6 +688,24 @@ struct tsv_ctx {
             throw StatusError(TSV_ECUDA, "schwarz2: potrf/potri failed");
     }
 
+    // Launch with programmatic stream serialisation (PDL) unless TSV_NO_PDL:
+    // the PCG iteration kernels (each starts with griddepcontrol.wait).
+    template <typename... KArgs, typename... Args>
+    void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+        static const bool off = getenv_flag("TSV_NO_PDL");
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = off ? 0 : 1;
+        CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+    }
+
     SolverHandles solver;   // created on first use, kept for the context's lifetime
     SolverHandles solver2;  // the coarse inverse's (worker thread, side stream)
 
@@ -1154,8 +1173,8 @@ struct tsv_ctx {
         tp.ZL = as2.ZL32.ptr;
         tp.ldz = static_cast<long long>(as2.LD);
         tp.done = &state.ptr->done;
-        tc_local_tf32_kernel<<<dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.mtiles)), kTcThreads,
-                               tc_smem_bytes(as2.BN), stream>>>(as2.tmA, as2.tmB, tp);
+        launch_pdl(tc_local_tf32_kernel, dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.mtiles)), kTcThreads,
+                   tc_smem_bytes(as2.BN), stream, as2.tmA, as2.tmB, tp);
     }
 
     size_t nn_count() const { return n / 3; }
@@ -1202,19 +1221,21 @@ struct tsv_ctx {
         // r update (grid-stride). Fusing the coarse restriction in (warp-level
         // per-cell partials) measured slower at config 3: 80 us vs 47 + 34 us
         // with the restriction off the critical path on the side stream.
-        as_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
         // fork: the coarse chain (cell sums of the restriction -> coarse rhs
         // -> coarse solve, HBM and latency bound) runs on a side stream beside
         // the local solves (tensor cores); both join before z. Captured as a
         // forked graph.
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(side, ev_fork, 0));
-        as_restrict_kernel<<<as2.ncells * kAsSplit, 256, 0, side>>>(q, a);
-        as_coarse_rhs_kernel<<<(as2.Nc + 255) / 256, 256, 0, side>>>(q, a);
+        launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 256, 0, side, q, a);
+        launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, side, q, a);
         if (as2.sym_nt) {
             const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
-            as_coarse_symv_kernel<<<ntiles, 128, 0, side>>>(q, a, as2.sym_tiles.ptr, as2.sym_nt, as2.sym_part.ptr);
-            as_coarse_symv_reduce_kernel<<<as2.sym_nt, kSymRedG * kSymT, 0, side>>>(q, a, as2.sym_nt, as2.sym_part.ptr);
+            launch_pdl(as_coarse_symv_kernel, ntiles, 128, 0, side, q, a, static_cast<const float *>(as2.sym_tiles.ptr),
+                       as2.sym_nt, as2.sym_part.ptr);
+            launch_pdl(as_coarse_symv_reduce_kernel, as2.sym_nt, kSymRedG * kSymT, 0, side, q, a, as2.sym_nt,
+                       static_cast<const double *>(as2.sym_part.ptr));
         } else {
             as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
             as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
@@ -1227,7 +1248,7 @@ struct tsv_ctx {
             gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
         }
         // the local part of z (and r.z_l) while the coarse chain finishes
-        as_zl_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a);
+        launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
         CK(cudaStreamWaitEvent(stream, ev_join, 0));
         launches += 7;
     }
@@ -1236,9 +1257,9 @@ struct tsv_ctx {
     void launch_scatter_p(const CgParams &q, int write_z = 0) {
         if (pre_kind == TSV_PRECOND_SCHWARZ2) {
             AsParams a = as_params();
-            as_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q, a, write_z);
+            launch_pdl(as_scatter_kernel, cg_grid(), kVecThreads, 0, stream, q, a, write_z);
         } else {
-            cg_scatter_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+            launch_pdl(cg_scatter_kernel, cg_grid(), kVecThreads, 0, stream, q);
         }
         ++launches;
     }
@@ -1408,12 +1429,12 @@ struct tsv_ctx {
             gp.n_tiles = static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
             gp.k_chunks = static_cast<int>(ldk / K1SmallCfg::KC);
             gp.tile_kind = tile_kind_small_d.ptr;
-            gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+            launch_pdl(gemm_nt_f64<K1SmallCfg>, k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream, gp);
         } else if (k1_streamk) {
             StreamK sk{sk_start.ptr, sk_work.ptr, sk_flag.ptr};
-            gemm_streamk_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp, sk);
+            launch_pdl(gemm_streamk_f64<K1Cfg>, k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream, gp, sk);
         } else {
-            gemm_nt_f64<K1Cfg><<<k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream>>>(gp);
+            launch_pdl(gemm_nt_f64<K1Cfg>, k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream, gp);
         }
         ++launches;
         CK(cudaGetLastError());
@@ -1446,11 +1467,11 @@ struct tsv_ctx {
 
     void launch_iteration(const CgParams &q) {
         launch_k1(&state.ptr->done);
-        cg_gather_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
         if (pre_kind == TSV_PRECOND_SCHWARZ2) {
             launch_as_update_precond(q);
         } else {
-            cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+            launch_pdl(cg_update_kernel, cg_grid(), kVecThreads, 0, stream, q);
             ++launches;
         }
         launch_scatter_p(q);

@@ -21,6 +21,15 @@ namespace tsvb200 {
 // C[m][n] = sum_k A[m][k] * Bt[n][k]  (+ row_scale[m] * col_bias[n]).
 // A: block-major operand panel, rows = blocks (GEMM row order), k contiguous.
 // Bt: K_r (symmetric, so K_r^T = K_r) or Phi (row-major [fine dof][k]).
+// Programmatic dependent launch: kernels of the PCG iteration are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs
+// are scheduled while its predecessor drains; griddepcontrol.wait holds them
+// until the predecessor's results are visible (a no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the dependent grid launch once every CTA of this one got here (its CTAs
+// then wait in pdl_wait until this grid's memory is visible).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct GemmParams {
     const double *A;
     long long lda;
@@ -216,6 +225,7 @@ __device__ __forceinline__ int gemm_fn_lim(const GemmParams &p, int nt) {
 // the streamed A panel in L2).
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParams p) {
+    pdl_wait();
     extern __shared__ __align__(16) double smem[];
     __shared__ int s_tile;
     double *As = smem;
@@ -241,6 +251,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
         gemm_segment<Cfg>(p, As, Bs, mt, nt, 0, p.k_chunks, gemm_fn_lim<Cfg>(p, nt), acc);
         gemm_epilogue<Cfg>(p, mt, nt, acc);
     }
+    pdl_trigger();
     // The last CTA out resets the tile counter for the next launch.
     if (tid == 0) {
         __threadfence();
@@ -269,6 +280,7 @@ struct StreamK {
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_streamk_f64(GemmParams p, StreamK sk) {
+    pdl_wait();
     extern __shared__ __align__(16) double smem[];
     double *As = smem;
     double *Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
@@ -439,6 +451,7 @@ __device__ __forceinline__ bool publish_partials(const double (&v)[NV], double *
 // A: Y (= A p or A x) summed per owned DoF; p'Ap or the true residual.
 // Grid-stride over nodes with a fixed grid (deterministic reduction).
 __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
+    pdl_wait();
     __shared__ double sh[64];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
@@ -471,6 +484,7 @@ __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
             }
         }
     }
+    pdl_trigger();
     block_sum<1>(part, sh);
     if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
     double tot[1];
@@ -503,6 +517,7 @@ __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
 // initial variants. The last CTA advances the iteration counter and
 // decides what the next operator product is (loop head of cg_solve).
 __global__ void __launch_bounds__(256) cg_update_kernel(CgParams q) {
+    pdl_wait();
     __shared__ double sh[64];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
@@ -591,6 +606,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(CgParams q) {
 // C: p = z + beta p (or p = z), then write the next operator operand (p,
 // or x for a verification) into the block-major panel, free DoFs only.
 __global__ void __launch_bounds__(256) cg_scatter_kernel(CgParams q) {
+    pdl_wait();
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
     const int p_assign = st->p_assign, yx = st->y_holds_x;

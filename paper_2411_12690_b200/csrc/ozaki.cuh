@@ -61,6 +61,7 @@ template <int S>
 __global__ void __launch_bounds__(256) oz_slice_kernel(const double *__restrict__ M, long long ldm, int rows, int ncols,
                                                        int8_t *__restrict__ planes, long long plane_rows, int KA,
                                                        int *__restrict__ ex, const int *done, const int *run_flag) {
+    pdl_wait();
     constexpr int kMaxGroups = 8;  // 4 values per lane per group: rows up to 1024 values
     if (done && *reinterpret_cast<const volatile int *>(done)) return;
     if (run_flag && !*reinterpret_cast<const volatile int *>(run_flag)) return;
@@ -159,6 +160,7 @@ template <int S>
 __global__ void __launch_bounds__(kTcThreads, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                    const __grid_constant__ CUtensorMap tmB1, OzParams p) {
+    pdl_wait();
     constexpr int BN = OzCfg<S>::BN;
     constexpr uint32_t A_TILE = kTcBM * kOzBK, B_TILE = BN * kOzBK;
     constexpr uint32_t STAGE = S * A_TILE + S * B_TILE;

@@ -115,6 +115,7 @@ __device__ __forceinline__ int as_corner_node(const AsParams &a, int cx, int cy,
 // max-iteration exit, next product = A x when the residual test passes).
 
 __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) {
+    pdl_wait();
     __shared__ double sh[64];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             }
         }
     }
+    pdl_trigger();
     block_sum<1>(part, sh);
     if (!publish_partials<1>(part, q.partial, &st->ticket_b)) return;
     double tot[1];
@@ -204,6 +206,7 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
 // Restriction, one CTA per super cell over its contiguous node range: the
 // cell's 24 partials of P^T r.
 __global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a) {
+    pdl_wait();
     __shared__ double sh[8][24];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int N = q.n_nodes;
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a
             for (int k = 0; k < 8; ++k) acc[3 * k + c] += w[k] * rv;
         }
     }
+    pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int k = 0; k < 24; ++k) {
@@ -241,6 +245,7 @@ __global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a
 
 // Coarse right-hand side: each coarse DoF sums its (up to 4) cells in order.
 __global__ void as_coarse_rhs_kernel(CgParams q, AsParams a) {
+    pdl_wait();
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= a.Nc) return;
@@ -267,6 +272,7 @@ constexpr int kGemvRows = 16;
 constexpr int kGemvChunk = 2048;
 
 __global__ void __launch_bounds__(256) as_coarse_gemv_kernel(CgParams q, AsParams a) {
+    pdl_wait();
     __shared__ double rcs[kGemvChunk];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -324,6 +330,7 @@ __device__ __forceinline__ void sym_tile_of(int t, int &I, int &J) {
 
 __global__ void __launch_bounds__(128) as_coarse_symv_kernel(CgParams q, AsParams a, const float *tiles, int NT,
                                                              double *part) {
+    pdl_wait();
     __shared__ double xi[kSymT], xj[kSymT];
     __shared__ double colp[8][kSymT];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
@@ -378,6 +385,7 @@ __global__ void __launch_bounds__(128) as_coarse_symv_kernel(CgParams q, AsParam
 constexpr int kSymRedG = 16;
 __global__ void __launch_bounds__(kSymRedG * kSymT) as_coarse_symv_reduce_kernel(CgParams q, AsParams a, int NT,
                                                                                const double *part) {
+    pdl_wait();
     __shared__ double sh[kSymRedG][kSymT];
     __shared__ double shd[64];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
@@ -430,6 +438,7 @@ __global__ void as_pack_sym_tiles_kernel(const double *A, int Nc, float *tiles, 
 
 // z_l and r.z_l (grid-stride, fixed grid; the last CTA stores rz_l).
 __global__ void __launch_bounds__(256) as_zl_kernel(CgParams q, AsParams a) {
+    pdl_wait();
     __shared__ double sh[64];
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
@@ -463,6 +472,7 @@ __global__ void __launch_bounds__(256) as_zl_kernel(CgParams q, AsParams a) {
             part[0] += rv * zv;
         }
     }
+    pdl_trigger();
     block_sum<1>(part, sh);
     if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
     double tot[1];
@@ -475,6 +485,7 @@ __global__ void __launch_bounds__(256) as_zl_kernel(CgParams q, AsParams a) {
 
 // rc.zc on the side stream (one CTA, fixed order).
 __global__ void __launch_bounds__(1024) as_coarse_dot_kernel(CgParams q, AsParams a) {
+    pdl_wait();
     __shared__ double sh[64];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     double v[1] = {0.0};
@@ -488,6 +499,7 @@ __global__ void __launch_bounds__(1024) as_coarse_dot_kernel(CgParams q, AsParam
 // verification) goes into the block-major panel (free DoFs). The last CTA
 // advances rho / phase. With write_z (tsv_precond_apply) z is stored too.
 __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a, int write_z) {
+    pdl_wait();
     __shared__ bool last;
     CgState *st = q.st;
     if (*reinterpret_cast<volatile int *>(&st->done)) return;
@@ -530,6 +542,7 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
             if (s.w >= 0) q.X[s.w + co] = v;
         }
     }
+    pdl_trigger();
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();

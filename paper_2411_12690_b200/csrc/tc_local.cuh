@@ -110,6 +110,7 @@ __device__ __forceinline__ float to_tf32(double v) {
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_local_tf32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcLocalParams p) {
+    pdl_wait();
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[kTcStages], empty_bar[kTcStages], accum_bar;
     __shared__ uint32_t tmem_slot;
