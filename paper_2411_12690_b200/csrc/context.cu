@@ -1389,9 +1389,9 @@ struct tsv_ctx {
     void launch_k1_oz(const int *done, const int *run_flag = nullptr) {
         constexpr int BN = OzCfg<S>::BN;
         const int KA = static_cast<int>(ldk);
-        oz_slice_kernel<S><<<static_cast<unsigned>(std::min<size_t>((B_pad + 7) / 8, static_cast<size_t>(sm_count) * 8)), 256, 0, stream>>>(
-            X.ptr, static_cast<long long>(ldk), static_cast<int>(B_pad), static_cast<int>(ldk), oz_a.ptr,
-            static_cast<long long>(B_pad), KA, oz_ea.ptr, done, run_flag);
+        launch_pdl(oz_slice_kernel<S>, static_cast<unsigned>(std::min<size_t>((B_pad + 7) / 8, static_cast<size_t>(sm_count) * 8)),
+                   256, 0, stream, static_cast<const double *>(X.ptr), static_cast<long long>(ldk), static_cast<int>(B_pad),
+                   static_cast<int>(ldk), oz_a.ptr, static_cast<long long>(B_pad), KA, oz_ea.ptr, done, run_flag);
         OzParams op{};
         op.tile_kind = tile_kind_d.ptr;
         op.a_plane_rows = static_cast<long long>(B_pad);
@@ -1408,8 +1408,8 @@ struct tsv_ctx {
         op.m_tiles = static_cast<int>(m_tiles);
         op.n_tiles = static_cast<int>(oz_brows / BN);
         const int tiles = op.m_tiles * op.n_tiles;
-        oz_gemm_kernel<S><<<static_cast<unsigned>(std::min(tiles, sm_count)), kTcThreads, oz_smem_bytes<S>(), stream>>>(
-            oz_tmA, oz_tmB[0], oz_tmB[1], op);
+        launch_pdl(oz_gemm_kernel<S>, static_cast<unsigned>(std::min(tiles, sm_count)), kTcThreads,
+                   static_cast<size_t>(oz_smem_bytes<S>()), stream, oz_tmA, oz_tmB[0], oz_tmB[1], op);
         launches += 2;
         CK(cudaGetLastError());
     }
