@@ -501,6 +501,22 @@ struct tsv_ctx {
         }
     }
 
+    // f(r) for r in [0, rows) on the host threads (rows are independent).
+    template <typename F>
+    static void parallel_rows(uint32_t rows, F &&f) {
+        const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), rows));
+        if (nt == 1) {
+            for (uint32_t r = 0; r < rows; ++r) f(r);
+            return;
+        }
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < nt; ++w)
+            pool.emplace_back([&, w] {
+                for (uint32_t r = w; r < rows; r += nt) f(r);
+            });
+        for (auto &t : pool) t.join();
+    }
+
     static bool getenv_flag(const char *name) {
         const char *v = std::getenv(name);
         return v && *v && *v != '0';
@@ -777,6 +793,23 @@ struct tsv_ctx {
         std::vector<double> Pall[2];  // per kind, column-major n x 24 each
         int nkind_keys[2] = {0, 0};
         const auto &snodes = nl.surface_nodes;
+        // per-cell keys on host threads (the constrained scan is B x n random
+        // reads), then numbered serially in cell order (deterministic ids)
+        std::vector<std::vector<long>> keys(B);
+        parallel_rows(rows, [&](uint32_t r) {
+            for (uint32_t c = 0; c < cols; ++c) {
+                const size_t cell = static_cast<size_t>(r) * cols + c;
+                const uint32_t *dm = dofmap.data() + cell * n;
+                const int cx = static_cast<int>(c) / sb, cy = static_cast<int>(r) / sb;
+                const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step;
+                const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step, index.lat_y - 1);
+                const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (q - 1);
+                std::vector<long> &key = keys[cell];
+                key = {layout.kind_at(cell), bx - x0, x1 - x0, by - y0, y1 - y0};
+                for (size_t a = 0; a < n; ++a)
+                    if (constrained[dm[a]]) key.push_back(static_cast<long>(a));
+            }
+        });
         for (uint32_t r = 0; r < rows; ++r)
             for (uint32_t c = 0; c < cols; ++c) {
                 const size_t cell = static_cast<size_t>(r) * cols + c;
@@ -785,9 +818,7 @@ struct tsv_ctx {
                 const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step;
                 const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step, index.lat_y - 1);
                 const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (q - 1);
-                std::vector<long> key = {layout.kind_at(cell), bx - x0, x1 - x0, by - y0, y1 - y0};
-                for (size_t a = 0; a < n; ++a)
-                    if (constrained[dm[a]]) key.push_back(static_cast<long>(a));
+                const std::vector<long> &key = keys[cell];
                 auto it = key_id.find(key);
                 if (it == key_id.end()) {
                     it = key_id.emplace(key, static_cast<int>(key_kind.size())).first;
@@ -937,10 +968,11 @@ struct tsv_ctx {
         const bool exact_types = getenv_flag("TSV_AS_EXACT_TYPES");
         std::map<std::vector<int>, int> sig_type;
         std::vector<int> type_of(B), rep_of;
-        for (uint32_t r = 0; r < rows; ++r)
+        std::vector<std::vector<int>> sigs(B);
+        parallel_rows(rows, [&](uint32_t r) {
             for (uint32_t c = 0; c < cols; ++c) {
                 const size_t cell = static_cast<size_t>(r) * cols + c;
-                std::vector<int> sig;
+                std::vector<int> &sig = sigs[cell];
                 sig.push_back(layout.kind_at(cell));
                 for (int dr = -1; dr <= 1; ++dr)
                     for (int dc = -1; dc <= 1; ++dc) {
@@ -953,6 +985,12 @@ struct tsv_ctx {
                 const uint32_t *dm = dofmap.data() + cell * n;
                 for (size_t a = 0; a < n; ++a)
                     if (constrained[dm[a]]) sig.push_back(1000 + static_cast<int>(a));
+            }
+        });
+        for (uint32_t r = 0; r < rows; ++r)
+            for (uint32_t c = 0; c < cols; ++c) {
+                const size_t cell = static_cast<size_t>(r) * cols + c;
+                const std::vector<int> &sig = sigs[cell];
                 auto it = sig_type.find(sig);
                 if (it == sig_type.end()) {
                     it = sig_type.emplace(sig, static_cast<int>(rep_of.size())).first;
