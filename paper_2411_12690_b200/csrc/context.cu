@@ -1266,7 +1266,7 @@ struct tsv_ctx {
         // forked graph.
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(side, ev_fork, 0));
-        launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 256, 0, side, q, a);
+        launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 3 * kRestrictGroup, 0, side, q, a);
         launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, side, q, a);
         if (as2.sym_nt) {
             const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;

@@ -205,40 +205,44 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
 
 // Restriction, one CTA per super cell over its contiguous node range: the
 // cell's 24 partials of P^T r.
-__global__ void __launch_bounds__(256) as_restrict_kernel(CgParams q, AsParams a) {
+// One CTA per coarse cell, kRestrictGroup threads per displacement component
+// (thread group c accumulates the 8 corner sums of component c: 8 registers
+// instead of 24, so more warps stay resident in this latency-bound pass).
+constexpr int kRestrictGroup = 128;
+__global__ void __launch_bounds__(3 * kRestrictGroup) as_restrict_kernel(CgParams q, AsParams a) {
     pdl_wait();
-    __shared__ double sh[8][24];
+    __shared__ double sh[3 * kRestrictGroup / 32][8];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int N = q.n_nodes;
     const int cell = blockIdx.x / kAsSplit;
     const AsCell cc = as_cell(a, cell);
     int nb, ne;
     as_part_range(a, cell, blockIdx.x % kAsSplit, nb, ne);
-    double acc[24];
+    const int c = threadIdx.x / kRestrictGroup, lt = threadIdx.x % kRestrictGroup;
+    double acc[8];
 #pragma unroll
-    for (int k = 0; k < 24; ++k) acc[k] = 0.0;
-    for (int node = nb + threadIdx.x; node < ne; node += blockDim.x) {
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+    for (int node = nb + lt; node < ne; node += kRestrictGroup) {
+        const long long dof = static_cast<long long>(c) * N + node;
+        const double rv = q.cmask[dof] ? 0.0 : q.r[dof];
         double w[8];
         as_cell_weights(a, cc, node, w);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const long long dof = static_cast<long long>(c) * N + node;
-            const double rv = q.cmask[dof] ? 0.0 : q.r[dof];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) acc[3 * k + c] += w[k] * rv;
-        }
+        for (int k = 0; k < 8; ++k) acc[k] += w[k] * rv;
     }
     pdl_trigger();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int k = 0; k < 24; ++k) {
+    for (int k = 0; k < 8; ++k) {
         const double v = warp_sum(acc[k]);
         if (lane == 0) sh[warp][k] = v;
     }
     __syncthreads();
-    if (threadIdx.x < 24) {
+    if (threadIdx.x < 24) {  // entry 3 k + c: component c's warps, in order
+        const int k = threadIdx.x / 3, cc2 = threadIdx.x % 3;
+        constexpr int wpg = kRestrictGroup / 32;
         double t = 0.0;
-        for (int w2 = 0; w2 < static_cast<int>(blockDim.x >> 5); ++w2) t += sh[w2][threadIdx.x];
+        for (int w2 = 0; w2 < wpg; ++w2) t += sh[cc2 * wpg + w2][k];
         a.cellpart[blockIdx.x * 24 + threadIdx.x] = t;  // [cell][part][24]
     }
 }
