@@ -62,27 +62,44 @@ GlobalIndex index_global_nodes(const ArrayLayout& layout, const NodeLayout& node
     const std::size_t slots = static_cast<std::size_t>(idx.lat_x) * idx.lat_y * idx.lat_z;
     if (slots >= 0x7fffffffULL) throw Error("index_global_nodes: lattice too large for 32-bit node ids");
     idx.node_of_lattice.assign(slots, -1);
-    {
-        // node count: every lattice point on an x- or y-face plane, plus the
-        // interior points of the bottom/top planes
-        const std::size_t fx = layout.cols + 1, fy = layout.rows + 1;
-        const std::size_t on_xy = fx * idx.lat_y + fy * idx.lat_x - fx * fy;
-        idx.lattice_of_node.reserve(on_xy * idx.lat_z + 2 * (static_cast<std::size_t>(idx.lat_x) * idx.lat_y - on_xy));
-    }
     // A lattice point is skipped only when it is off every block face plane
-    // in x and in y and off the top/bottom planes.
-    for (std::uint32_t gz = 0; gz < idx.lat_z; ++gz) {
+    // in x and in y and off the top/bottom planes. Nodes are numbered in scan
+    // order gz -> gy -> gx: count the kept points per (gz, gy) line, prefix-sum,
+    // then number the lines independently on the host threads (same ids).
+    const std::size_t lines = static_cast<std::size_t>(idx.lat_z) * idx.lat_y;
+    auto keep = [&](std::uint32_t gx, std::uint32_t gy, std::uint32_t gz) {
         const bool on_z_face = gz == 0 || gz + 1 == idx.lat_z;
-        for (std::uint32_t gy = 0; gy < idx.lat_y; ++gy) {
-            const bool on_y_face = gy % (idx.ny - 1) == 0;
+        const bool on_y_face = gy % (idx.ny - 1) == 0;
+        const bool on_x_face = gx % (idx.nx - 1) == 0;
+        return on_x_face || on_y_face || on_z_face;
+    };
+    std::vector<std::size_t> first(lines + 1, 0);
+    const std::size_t x_faces = layout.cols + 1;  // kept points of a line off every y/z face plane
+    for (std::size_t l = 0; l < lines; ++l) {
+        const std::uint32_t gz = static_cast<std::uint32_t>(l / idx.lat_y), gy = static_cast<std::uint32_t>(l % idx.lat_y);
+        const bool full = gz == 0 || gz + 1 == idx.lat_z || gy % (idx.ny - 1) == 0;
+        first[l + 1] = first[l] + (full ? idx.lat_x : x_faces);
+    }
+    idx.lattice_of_node.resize(first[lines]);
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 16u));
+    auto work = [&](unsigned w) {
+        for (std::size_t l = w; l < lines; l += nt) {
+            const std::uint32_t gz = static_cast<std::uint32_t>(l / idx.lat_y), gy = static_cast<std::uint32_t>(l % idx.lat_y);
+            std::size_t id = first[l];
             for (std::uint32_t gx = 0; gx < idx.lat_x; ++gx) {
-                const bool on_x_face = gx % (idx.nx - 1) == 0;
-                if (!on_x_face && !on_y_face && !on_z_face) continue;
-                idx.node_of_lattice[idx.lattice_slot(gx, gy, gz)] =
-                    static_cast<std::int32_t>(idx.lattice_of_node.size());
-                idx.lattice_of_node.push_back({gx, gy, gz});
+                if (!keep(gx, gy, gz)) continue;
+                idx.node_of_lattice[idx.lattice_slot(gx, gy, gz)] = static_cast<std::int32_t>(id);
+                idx.lattice_of_node[id] = {gx, gy, gz};
+                ++id;
             }
         }
+    };
+    if (nt == 1 || slots < (1u << 16)) {
+        for (unsigned w = 0; w < nt; ++w) work(w);
+    } else {
+        std::vector<std::thread> pool;
+        for (unsigned w = 0; w < nt; ++w) pool.emplace_back(work, w);
+        for (auto& t : pool) t.join();
     }
     if (idx.dof_count() >= 0xffffffffULL) throw Error("index_global_nodes: more than 2^32 reduced dofs");
     return idx;
