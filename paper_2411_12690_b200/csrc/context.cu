@@ -708,7 +708,7 @@ struct tsv_ctx {
     // the PCG iteration kernels (each starts with griddepcontrol.wait).
     template <typename... KArgs, typename... Args>
     void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
-        static const bool off = getenv_flag("TSV_NO_PDL");
+        const bool off = getenv_flag("TSV_NO_PDL");  // read per launch (graph capture, run_cg prologue)
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
         cfg.blockDim = block;

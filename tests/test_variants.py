@@ -108,3 +108,21 @@ def test_nonzero_dirichlet_lifting_rigid_translation(oracle_libs, native_lib):
     mx, _ = stress_errors(g.recover(8), s0)
     assert mx.max() <= 1e-7
     g.close()
+
+
+def test_programmatic_dependent_launch_is_bitwise_neutral(oracle_libs, native_lib, monkeypatch):
+    """PDL only changes when CTAs are scheduled, never what they compute:
+    the Schwarz solve is bitwise identical with TSV_NO_PDL=1."""
+    refpy, _ = oracle_libs
+    out = []
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("TSV_NO_PDL", flag)
+        else:
+            monkeypatch.delenv("TSV_NO_PDL", raising=False)
+        sess, g = _mixed(refpy)
+        sol = g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
+        out.append((sol.u, sol.iterations))
+        g.close()
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][0], out[1][0])
