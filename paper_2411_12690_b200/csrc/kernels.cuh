@@ -823,9 +823,20 @@ __global__ void __launch_bounds__(256) k6_face_kernel(K6Face p) {
     if (t0 >= nrows) return;
     const int tid = threadIdx.x;
     const double *wt = p.gwt + p.gwoff[blockIdx.y];
-    for (int i = tid; i < K * 128; i += 256) {
-        const int k = i >> 7, j = i & 127;
-        ws[k][j] = t0 + j < nrows ? wt[static_cast<long long>(k) * nrows + t0 + j] : 0.0;
+    // staging loads issued in batches of 8 before their stores (one memory
+    // round trip per batch instead of one per element)
+    for (int i0 = tid; i0 < K * 128; i0 += 256 * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + 256 * u, k = i >> 7, j = i & 127;
+            v[u] = (i < K * 128 && t0 + j < nrows) ? wt[static_cast<long long>(k) * nrows + t0 + j] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + 256 * u;
+            if (i < K * 128) ws[i >> 7][i & 127] = v[u];
+        }
     }
     const int gq = tid & 31, bq = tid >> 5;  // group rows gq + 32 b (coalesced stores), block rows 4 bq + a
     int dof[4];
@@ -836,15 +847,29 @@ __global__ void __launch_bounds__(256) k6_face_kernel(K6Face p) {
         dof[b] = j < nrows ? p.gdof[row_off + j] : -1;
         ut[b] = j < nrows ? p.ut[dof[b]] : 0.0;
     }
+    // X gathers of the next 32-row sub-tile are issued before the current
+    // one is computed (register double buffer)
+    static_assert(kFaceK * 32 <= 256 * 8, "one batch of gathers per sub-tile");
+    double v[8];
+    auto gather = [&](int r0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = tid + 256 * u, k = i >> 5, r = i & 31;
+            v[u] = (i < K * 32 && r0 + r < p.rows) ? p.X[(static_cast<long long>(r0) + r) * p.ldk + p.gcol[col_off + k]] : 0.0;
+        }
+    };
+    gather(blockIdx.x * kFaceSub * 32);
     for (int sub = 0; sub < kFaceSub; ++sub) {
         const int r0 = (blockIdx.x * kFaceSub + sub) * 32;
         if (r0 >= p.rows) break;
         __syncthreads();  // ws staged / previous sub-tile's qs consumed
-        for (int i = tid; i < K * 32; i += 256) {
-            const int k = i >> 5, r = i & 31;
-            qs[k][r] = r0 + r < p.rows ? p.X[(static_cast<long long>(r0) + r) * p.ldk + p.gcol[col_off + k]] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = tid + 256 * u;
+            if (i < K * 32) qs[i >> 5][i & 31] = v[u];
         }
         __syncthreads();
+        if (sub + 1 < kFaceSub) gather(r0 + 32);
         double acc[4][4];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
