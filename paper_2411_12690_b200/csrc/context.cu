@@ -1283,7 +1283,8 @@ struct tsv_ctx {
             launch_tc_local();
         } else {
             GemmParams gp = local_gemm_params();
-            gemm_nt_f64<K1SmallCfg><<<k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream>>>(gp);
+            gemm_nt_f64<K1SmallCfg><<<std::min(k1s_grid, gp.m_tiles * gp.n_tiles), K1SmallCfg::THREADS, K1SmallCfg::SMEM,
+                                      stream>>>(gp);
         }
         // the local part of z (and r.z_l) while the coarse chain finishes
         launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
@@ -1467,12 +1468,15 @@ struct tsv_ctx {
             gp.n_tiles = static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
             gp.k_chunks = static_cast<int>(ldk / K1SmallCfg::KC);
             gp.tile_kind = tile_kind_small_d.ptr;
-            launch_pdl(gemm_nt_f64<K1SmallCfg>, k1s_grid, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream, gp);
+            // no more CTAs than tiles: idle CTAs would only contend on the tile counter
+            const int g = std::min(k1s_grid, gp.m_tiles * gp.n_tiles);
+            launch_pdl(gemm_nt_f64<K1SmallCfg>, g, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream, gp);
         } else if (k1_streamk) {
             StreamK sk{sk_start.ptr, sk_work.ptr, sk_flag.ptr};
             launch_pdl(gemm_streamk_f64<K1Cfg>, k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream, gp, sk);
         } else {
-            launch_pdl(gemm_nt_f64<K1Cfg>, k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream, gp);
+            launch_pdl(gemm_nt_f64<K1Cfg>, std::min(k1_grid, gp.m_tiles * gp.n_tiles), K1Cfg::THREADS, K1Cfg::SMEM,
+                       stream, gp);
         }
         ++launches;
         CK(cudaGetLastError());
@@ -1676,7 +1680,7 @@ struct tsv_ctx {
         gp.n_major = 1;
         gp.col_map = mk.n_dense < mk.n_fine ? mk.d_dmap.ptr : nullptr;
         if (mk.n_dense) {
-            gemm_nt_f64<K6Cfg><<<k6_grid, K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
+            gemm_nt_f64<K6Cfg><<<std::min(k6_grid, gp.m_tiles * gp.n_tiles), K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
             ++launches;
         }
         if (mk.n_groups) {
