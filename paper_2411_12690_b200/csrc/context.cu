@@ -42,8 +42,18 @@ using namespace tsvb200;
 
 namespace {
 
-using K1Cfg = GemmCfg<128, 64, 2, 2, 16, 3>;
-using K6Cfg = GemmCfg<128, 64, 2, 2, 16, 3>;
+// K1 tile configuration (BM, BN, warps M x N, KC, stages, CTAs per SM). Measured
+// at configs 3 / 4 (ms per launch): 2x2 warps 0.289 / 0.254; 4x1 warps 0.285 /
+// 0.248 (default); 4 stages 0.395 / 0.351; 2 stages 0.293 / 0.255; 8x1 warps
+// (1 CTA/SM) 0.342 / 0.299; 4x2 warps (1 CTA/SM) 0.340 / 0.305.
+#ifndef TSV_K1CFG
+#define TSV_K1CFG 128, 64, 4, 1, 16, 3, 2
+#endif
+#ifndef TSV_K6CFG  // K6 (recovery GEMM), same shape family: 4x1 warps 16.33 ms vs 2x2 16.60 ms recovery at config 3
+#define TSV_K6CFG 128, 64, 4, 1, 16, 3, 2
+#endif
+using K1Cfg = GemmCfg<TSV_K1CFG>;
+using K6Cfg = GemmCfg<TSV_K6CFG>;
 using K1SmallCfg = GemmCfg<64, 64, 2, 2, 16, 3, 3>;  // KC must divide ldk (multiple of 16)
 constexpr int kBM = K1Cfg::BM;
 constexpr int kBN = K1Cfg::BN;
@@ -1955,6 +1965,8 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1Cfg::SMEM)));
+        CK(cudaFuncSetAttribute(gemm_nt_f64<K6Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K6Cfg::SMEM)));
         CK(cudaFuncSetAttribute(gemm_streamk_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1Cfg::SMEM)));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1SmallCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1965,7 +1977,10 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         ctx->k1s_grid = std::max(1, occ_s) * ctx->sm_count;
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_nt_f64<K1Cfg>, K1Cfg::THREADS, K1Cfg::SMEM));
-        ctx->k1_grid = ctx->k6_grid = std::max(1, occ) * ctx->sm_count;
+        ctx->k1_grid = std::max(1, occ) * ctx->sm_count;
+        int occ6 = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ6, gemm_nt_f64<K6Cfg>, K6Cfg::THREADS, K6Cfg::SMEM));
+        ctx->k6_grid = std::max(1, occ6) * ctx->sm_count;
         int occ_sk = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sk, gemm_streamk_f64<K1Cfg>, K1Cfg::THREADS, K1Cfg::SMEM));
         ctx->sk_resident = occ_sk * ctx->sm_count >= ctx->k1_grid;  // stream-K waits need every CTA resident
