@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(3 * kRestrictGroup) as_restrict_kernel(CgParam
     for (int k = 0; k < 8; ++k) acc[k] = 0.0;
     for (int node = nb + lt; node < ne; node += kRestrictGroup) {
         const long long dof = static_cast<long long>(c) * N + node;
-        const double rv = q.cmask[dof] ? 0.0 : q.r[dof];
+        const double r0 = __ldg(q.r + dof);  // loaded unconditionally: no cmask -> r dependency
+        const double rv = __ldg(q.cmask + dof) ? 0.0 : r0;
         double w[8];
         as_cell_weights(a, cc, node, w);
 #pragma unroll
