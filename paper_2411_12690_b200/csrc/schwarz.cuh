@@ -528,13 +528,13 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
             const long long dof = static_cast<long long>(c) * N + node;
             double zv = a.z[dof];
             const bool cm = q.cmask[dof] != 0;
-            if (!cm) {
+            double zcoarse = 0.0;  // computed whether or not the DoF is constrained (no cmask -> zc dependency)
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
-                    zv += w * __ldg(a.zc + 3 * as_corner_node(a, cx, cy, k) + c);
-                }
+            for (int k = 0; k < 8; ++k) {
+                const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
+                zcoarse += w * __ldg(a.zc + 3 * as_corner_node(a, cx, cy, k) + c);
             }
+            if (!cm) zv += zcoarse;
             if (write_z) a.z[dof] = zv;
             const double pn = normal ? zv + beta * q.p[dof] : zv;
             q.p[dof] = pn;
