@@ -1438,7 +1438,10 @@ struct tsv_ctx {
     void launch_k1_oz(const int *done, const int *run_flag = nullptr) {
         constexpr int BN = OzCfg<S>::BN;
         const int KA = static_cast<int>(ldk);
-        launch_pdl(oz_slice_kernel<S>, static_cast<unsigned>(std::min<size_t>((B_pad + 7) / 8, static_cast<size_t>(sm_count) * 8)),
+        // with a run flag (the true-residual check) the launch is usually an
+        // early exit: one CTA per SM keeps that cheap
+        const size_t slice_ctas = static_cast<size_t>(sm_count) * (run_flag ? 1 : 8);
+        launch_pdl(oz_slice_kernel<S>, static_cast<unsigned>(std::min<size_t>((B_pad + 7) / 8, slice_ctas)),
                    256, 0, stream, static_cast<const double *>(X.ptr), static_cast<long long>(ldk), static_cast<int>(B_pad),
                    static_cast<int>(ldk), oz_a.ptr, static_cast<long long>(B_pad), KA, oz_ea.ptr, done, run_flag);
         OzParams op{};
