@@ -126,3 +126,20 @@ def test_programmatic_dependent_launch_is_bitwise_neutral(oracle_libs, native_li
         g.close()
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][0], out[1][0])
+
+
+def test_recover_into_pinned_host_memory(oracle_libs, native_lib):
+    """tsv_host_alloc result buffers (the bench e2e path) receive the same
+    stress as a pageable numpy array, across the double-buffered D2H."""
+    import ctypes as C
+    from paper_2411_12690_b200.api import PinnedArray
+    refpy, _ = oracle_libs
+    sess, g = _mixed(refpy)
+    g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
+    s_np = g.recover(8)
+    pin = PinnedArray(s_np.shape)
+    rc = g._L.tsv_recover(g._h, 8, 0, s_np.shape[0], pin.array.ctypes.data_as(C.c_void_p))
+    assert rc == 0
+    assert np.array_equal(pin.array, s_np)
+    pin.close()
+    g.close()
