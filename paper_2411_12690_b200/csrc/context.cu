@@ -254,6 +254,8 @@ struct tsv_ctx {
         bool tc = false;
         int KP = 0, NP = 0, BN = 0, ntn = 0, LD = 0;  // LD: row stride of XL32 and ZL
         DevBuf<float> XL32, ainv32, ZL32;
+        DevBuf<int2> tc_pairs;  // consecutive same-type M tiles for tc_local_pair_kernel
+        int npairs = 0;
         CUtensorMap tmA{}, tmB{};
         DevBuf<float> ainv_c32;
         int ldc32 = 0;
@@ -1114,6 +1116,22 @@ struct tsv_ctx {
         as2.mtiles = row / BML;
         if (as2.BL_pad * ldk >= 0x7fffffffULL) throw StatusError(TSV_EINVAL, "schwarz2: panel too large");
         as2.tile_type.upload(tiles.data(), tiles.size(), stream);
+        {
+            std::vector<int2> pr;
+            for (size_t i = 0; i < tiles.size();) {
+                if (i + 1 < tiles.size() && tiles[i + 1] == tiles[i]) {
+                    pr.push_back(make_int2(static_cast<int>(i), static_cast<int>(i + 1)));
+                    i += 2;
+                } else {
+                    pr.push_back(make_int2(static_cast<int>(i), -1));
+                    i += 1;
+                }
+            }
+            const bool use_pairs = as2.tc && as2.BN <= 256 && !getenv_flag("TSV_TC_SINGLE") &&
+                                   tc_pair_smem_bytes(as2.BN) <= 227 * 1024;
+            as2.npairs = use_pairs ? static_cast<int>(pr.size()) : 0;
+            if (use_pairs) as2.tc_pairs.upload(pr.data(), pr.size(), stream);
+        }
         std::vector<int> s2(nodes * 4, -1);
         for (size_t cell = 0; cell < B; ++cell) {
             const uint32_t *dm = dofmap.data() + cell * n;
@@ -1208,6 +1226,8 @@ struct tsv_ctx {
         static bool attr = false;
         if (!attr) {
             CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
+            CK(cudaFuncSetAttribute(tc_local_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    tc_pair_smem_bytes(256)));
             attr = true;
         }
     }
@@ -1221,8 +1241,14 @@ struct tsv_ctx {
         tp.ZL = as2.ZL32.ptr;
         tp.ldz = static_cast<long long>(as2.LD);
         tp.done = &state.ptr->done;
-        launch_pdl(tc_local_tf32_kernel, dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.mtiles)), kTcThreads,
-                   tc_smem_bytes(as2.BN), stream, as2.tmA, as2.tmB, tp);
+        if (as2.npairs) {
+            launch_pdl(tc_local_pair_kernel, dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.npairs)),
+                       kTcThreads, tc_pair_smem_bytes(as2.BN), stream, as2.tmA, as2.tmB, tp,
+                       static_cast<const int2 *>(as2.tc_pairs.ptr));
+        } else {
+            launch_pdl(tc_local_tf32_kernel, dim3(static_cast<unsigned>(as2.ntn), static_cast<unsigned>(as2.mtiles)),
+                       kTcThreads, tc_smem_bytes(as2.BN), stream, as2.tmA, as2.tmB, tp);
+        }
     }
 
     size_t nn_count() const { return n / 3; }
