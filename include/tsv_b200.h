@@ -120,6 +120,14 @@ int tsv_save_rom_file(const tsv_rom_desc *rom, int kind, const char *path, char 
 int tsv_set_layout(tsv_ctx *ctx, uint32_t rows, uint32_t cols, const uint8_t *kinds,
                    const double *delta_t, size_t n_delta_t, double pitch, double height);
 
+/* Online update of the per-block temperature change only (ArrayLayout::
+ * delta_t, global.hpp:16-32; the thermal load b[dof] += dT_b b_el[a],
+ * global_stage.cpp:135-142, and the recovery's dT_b u_T term,
+ * global_stage.cpp:215-230). Keeps the index, dof map, Dirichlet set and
+ * the preconditioner (which depends on kinds and BCs only); the load is
+ * re-assembled on the device by the next solve. 1 or rows*cols entries. */
+int tsv_set_delta_t(tsv_ctx *ctx, const double *delta_t, size_t n_delta_t);
+
 /* Dirichlet data: a fem::DirichletSet (fem.hpp:22-36) given as sorted or
  * unsorted (dof, value) pairs, or one of the tsv_bc_kind sets. Lifting
  * follows apply_dirichlet_lifting (fem.cpp:223-260). */

@@ -148,17 +148,7 @@ public:
     /// argument (tolerance, max_iterations, precond).
     template <class Opts = IterOptions>
     GlobalSolution solve_global(const Opts &o = Opts{}) {
-        tsv_iter_options c{o.tolerance, o.max_iterations, static_cast<int>(o.precond)};
-        GlobalSolution sol;
-        sol.u.resize(dof_count());
-        tsv_solve_info info{};
-        const int rc = tsv_solve(ctx_, &c, sol.u.data(), &info);
-        sol.iterations = info.iterations;
-        sol.relative_residual = info.relative_residual;
-        sol.device_ms = info.solve_ms;
-        if (rc == TSV_ENOCONV) throw NoConvergence(std::move(sol), tsv_last_error(ctx_));
-        check(rc);
-        return sol;
+        return solve_with(o, static_cast<int>(o.precond));
     }
 
     /// The same solve with a preconditioner outside linalg::Precond, e.g.
@@ -166,17 +156,13 @@ public:
     /// parity bar, far fewer iterations).
     template <class Opts = IterOptions>
     GlobalSolution solve_global(const Opts &o, int precond_override) {
-        tsv_iter_options c{o.tolerance, o.max_iterations, precond_override};
-        GlobalSolution sol;
-        sol.u.resize(dof_count());
-        tsv_solve_info info{};
-        const int rc = tsv_solve(ctx_, &c, sol.u.data(), &info);
-        sol.iterations = info.iterations;
-        sol.relative_residual = info.relative_residual;
-        sol.device_ms = info.solve_ms;
-        if (rc == TSV_ENOCONV) throw NoConvergence(std::move(sol), tsv_last_error(ctx_));
-        check(rc);
-        return sol;
+        return solve_with(o, precond_override);
+    }
+
+    /// Online stage with a new temperature field only (ArrayLayout::delta_t,
+    /// global.hpp:16-32): index, BCs and the preconditioner are kept.
+    void set_delta_t(const std::vector<double> &delta_t) {
+        check(tsv_set_delta_t(ctx_, delta_t.data(), delta_t.size()));
     }
 
     /// rom::load_rom (rom.cpp:305-377) straight into a RomSet slot (-1 = the
@@ -217,6 +203,21 @@ public:
     tsv_ctx *handle() { return ctx_; }
 
 private:
+    template <class Opts>
+    GlobalSolution solve_with(const Opts &o, int precond) {
+        tsv_iter_options c{o.tolerance, o.max_iterations, precond};
+        GlobalSolution sol;
+        sol.u.resize(dof_count());
+        tsv_solve_info info{};
+        const int rc = tsv_solve(ctx_, &c, sol.u.data(), &info);
+        sol.iterations = info.iterations;
+        sol.relative_residual = info.relative_residual;
+        sol.device_ms = info.solve_ms;
+        if (rc == TSV_ENOCONV) throw NoConvergence(std::move(sol), tsv_last_error(ctx_));
+        check(rc);
+        return sol;
+    }
+
     void check(int rc) {
         if (rc == TSV_OK) return;
         const std::string msg = tsv_last_error(ctx_);

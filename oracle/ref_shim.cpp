@@ -77,8 +77,17 @@ const char* ref_last_error() { return g_err.c_str(); }
 /// build_rom (rom.cpp:134-253) on a uniform TensorGrid (linspace, as the
 /// reference fixtures do, test_global.cpp:22-28) with the default materials
 /// (material.cpp:37-43) except the liner Young modulus.
+void* ref_rom_build3(double d, double h, double t, double p, int m_xy, int m_z, int qx, int qy, int qz,
+                     int kind, double liner_e, int threads);
+
 void* ref_rom_build(double d, double h, double t, double p, int m_xy, int m_z, int q, int kind,
                     double liner_e, int threads) {
+    return ref_rom_build3(d, h, t, p, m_xy, m_z, q, q, q, kind, liner_e, threads);
+}
+
+// NodeLayout with separate node counts per axis (rom::NodeLayout::create(nx, ny, nz, ...)).
+void* ref_rom_build3(double d, double h, double t, double p, int m_xy, int m_z, int qx, int qy, int qz,
+                     int kind, double liner_e, int threads) {
     Rom* out = nullptr;
     int st = guarded([&] {
         UnitBlockGeometry g;
@@ -90,7 +99,7 @@ void* ref_rom_build(double d, double h, double t, double p, int m_xy, int m_z, i
         MaterialTable mats = MaterialTable::defaults();
         const Material& l = mats[MaterialId::Liner];
         mats[MaterialId::Liner] = Material::make(liner_e, l.poisson_ratio, l.thermal_expansion);
-        rom::NodeLayout nl = rom::NodeLayout::create(q, q, q, p, p, h);
+        rom::NodeLayout nl = rom::NodeLayout::create(qx, qy, qz, p, p, h);
         BlockKind k = kind == 0 ? BlockKind::Tsv : BlockKind::Dummy;
         HexMesh mesh = k == BlockKind::Tsv ? build_unit_block_mesh(g, grid) : build_dummy_block_mesh(g, grid);
         out = new Rom{rom::build_rom(g, mesh, mats, nl, k, threads)};

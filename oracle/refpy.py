@@ -30,6 +30,8 @@ def lib():
         L.ref_last_error.restype = C.c_char_p
         L.ref_rom_build.restype = vp
         L.ref_rom_build.argtypes = [d, d, d, d, i, i, i, i, d, i]
+        L.ref_rom_build3.restype = vp
+        L.ref_rom_build3.argtypes = [d, d, d, d, i, i, i, i, i, i, d, i]
         L.ref_rom_load.restype = vp
         L.ref_rom_load.argtypes = [C.c_char_p]
         L.ref_rom_save.argtypes = [vp, C.c_char_p]
@@ -125,6 +127,8 @@ def build_rom(d, h, t, p, m_xy, m_z, q, kind=0, liner_e=71.7e9, threads=0):
     """rom::build_rom (rom.cpp:134-253) on a uniform grid."""
     if threads <= 0:
         threads = os.cpu_count() or 1
+    if not np.isscalar(q):  # NodeLayout (n_x, n_y, n_z)
+        return _wrap_rom(lib().ref_rom_build3(d, h, t, p, m_xy, m_z, *[int(v) for v in q], kind, liner_e, threads))
     return _wrap_rom(lib().ref_rom_build(d, h, t, p, m_xy, m_z, q, kind, liner_e, threads))
 
 

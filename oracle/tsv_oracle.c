@@ -197,6 +197,56 @@ void orc_apply(const orc_system *s, uint32_t rows, uint32_t cols, const double *
         if (s->constrained[i]) y[i] = x[i]; /* unit row, fem.cpp:240-245 */
 }
 
+/* r = b - A x with the block products and the sums in long double (x87,
+ * 64-bit mantissa), rounded once at the end. Only the oracle's
+ * true-residual check uses it (orc_cg_solve_pc with exact_residual): at
+ * configs 3/4 the FP64 rounding of A x alone is ~1e-12 relative to |b|,
+ * the solver tolerance, so an FP64 check restarts forever. */
+typedef struct {
+    const orc_system *s;
+    const size_t *blocks;
+    const double *x;
+    long double *y;
+} orc_apply_ld_ctx;
+
+static void orc_apply_ld_range(void *p, size_t begin, size_t end) {
+    orc_apply_ld_ctx *c = (orc_apply_ld_ctx *)p;
+    const orc_system *s = c->s;
+    const size_t n = s->n;
+    double *xb = malloc(n * sizeof(double));
+    for (size_t t = begin; t < end; ++t) {
+        size_t b = c->blocks[t];
+        const uint32_t *dm = s->dof_map + b * n;
+        const double *K = s->K[s->kinds ? s->kinds[b] : 0];
+        for (size_t a = 0; a < n; ++a) xb[a] = s->constrained[dm[a]] ? 0.0 : c->x[dm[a]];
+        for (size_t a = 0; a < n; ++a) {
+            if (s->constrained[dm[a]]) continue;
+            const double *row = K + a * n;
+            long double acc = 0.0L;
+            for (size_t k = 0; k < n; ++k) acc += (long double)row[k] * (long double)xb[k];
+            c->y[dm[a]] += acc;
+        }
+    }
+    free(xb);
+}
+
+void orc_residual_ld(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, const double *x,
+                     double *r) {
+    long double *y = calloc(s->N, sizeof(long double));
+    size_t *blocks = malloc(s->B * sizeof(size_t));
+    for (int colour = 0; colour < 4; ++colour) {
+        size_t nb = 0;
+        for (uint32_t rr = (uint32_t)(colour >> 1); rr < rows; rr += 2)
+            for (uint32_t cc = (uint32_t)(colour & 1); cc < cols; cc += 2) blocks[nb++] = (size_t)rr * cols + cc;
+        orc_apply_ld_ctx ctx = {s, blocks, x, y};
+        orc_parallel(nb, s->threads, orc_apply_ld_range, &ctx);
+    }
+    for (size_t i = 0; i < s->N; ++i)
+        r[i] = s->constrained[i] ? b[i] - x[i] : (double)((long double)b[i] - y[i]);
+    free(blocks);
+    free(y);
+}
+
 void orc_rhs(const orc_system *s, uint32_t rows, uint32_t cols, double *b) {
     (void)rows;
     (void)cols;
@@ -276,6 +326,7 @@ static double orc_sdot(const double *a, const double *b, size_t n) { /* linalg.c
 
 typedef struct {
     int kind;
+    size_t n;
     double *inv_diag;
     double *blocks;
 } orc_precond;
@@ -283,6 +334,7 @@ typedef struct {
 static void orc_precond_init(orc_precond *p, const orc_system *s, int kind) {
     /* Preconditioner ctor, linalg.cpp:223-262 */
     p->kind = kind;
+    p->n = s->N;
     p->inv_diag = NULL;
     p->blocks = NULL;
     size_t n = s->N;
@@ -342,8 +394,38 @@ static void orc_precond_apply(const orc_precond *p, const double *r, double *z, 
     }
 }
 
+static void orc_builtin_pc(void *ctx, const double *r, double *z) {
+    const orc_precond *p = (const orc_precond *)ctx;
+    orc_precond_apply(p, r, z, p->n);
+}
+
+static int orc_cg_core(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, double tol,
+                       int max_iterations, orc_pc_fn pc_fn, void *pc_ctx, int exact_residual, double *x,
+                       int *iterations, double *relres);
+
 int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, double tol,
                  int max_iterations, int precond, double *x, int *iterations, double *relres) {
+    orc_precond pc;
+    pc.kind = precond;
+    pc.n = s->N;
+    pc.inv_diag = NULL;
+    pc.blocks = NULL;
+    orc_precond_init(&pc, s, precond);
+    int st = orc_cg_core(s, rows, cols, b, tol, max_iterations, orc_builtin_pc, &pc, 0, x, iterations, relres);
+    free(pc.inv_diag);
+    free(pc.blocks);
+    return st;
+}
+
+int orc_cg_solve_pc(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, double tol,
+                    int max_iterations, orc_pc_fn pc, void *pc_ctx, int exact_residual, double *x, int *iterations,
+                    double *relres) {
+    return orc_cg_core(s, rows, cols, b, tol, max_iterations, pc, pc_ctx, exact_residual, x, iterations, relres);
+}
+
+static int orc_cg_core(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, double tol,
+                       int max_iterations, orc_pc_fn pc_fn, void *pc_ctx, int exact_residual, double *x,
+                       int *iterations, double *relres) {
     /* cg_solve, linalg.cpp:292-362 */
     const size_t n = s->N;
     const double norm_b = sqrt(orc_sdot(b, b, n));
@@ -354,8 +436,6 @@ int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double
         if (!isfinite(b[i])) return ORC_EBREAKDOWN; /* check_finite, linalg.cpp:215-218 */
     if (norm_b == 0.0) return ORC_OK;
 
-    orc_precond pc;
-    orc_precond_init(&pc, s, precond);
     double *r = malloc(n * sizeof(double)), *z = malloc(n * sizeof(double));
     double *p = malloc(n * sizeof(double)), *ap = malloc(n * sizeof(double));
     double *best_x = malloc(n * sizeof(double));
@@ -363,7 +443,7 @@ int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double
 
     orc_apply(s, rows, cols, x, r);
     for (size_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
-    orc_precond_apply(&pc, r, z, n);
+    pc_fn(pc_ctx, r, z);
     memcpy(p, z, n * sizeof(double));
     double rho = orc_sdot(r, z, n);
     double res_norm = sqrt(orc_sdot(r, r, n));
@@ -373,11 +453,15 @@ int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double
 
     while (it < max_iterations) {
         if (res_norm <= tol * norm_b) {
-            orc_apply(s, rows, cols, x, r);
-            for (size_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+            if (exact_residual) {
+                orc_residual_ld(s, rows, cols, b, x, r);
+            } else {
+                orc_apply(s, rows, cols, x, r);
+                for (size_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
+            }
             res_norm = sqrt(orc_sdot(r, r, n));
             if (res_norm <= tol * norm_b) break;
-            orc_precond_apply(&pc, r, z, n);
+            pc_fn(pc_ctx, r, z);
             memcpy(p, z, n * sizeof(double));
             rho = orc_sdot(r, z, n);
         }
@@ -390,7 +474,7 @@ int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double
         double alpha = rho / pap;
         for (size_t i = 0; i < n; ++i) x[i] += alpha * p[i];
         for (size_t i = 0; i < n; ++i) r[i] -= alpha * ap[i];
-        orc_precond_apply(&pc, r, z, n);
+        pc_fn(pc_ctx, r, z);
         double rho_next = orc_sdot(r, z, n);
         double beta = rho_next / rho;
         rho = rho_next;
@@ -415,7 +499,6 @@ int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double
     }
 done:
     free(r); free(z); free(p); free(ap); free(best_x);
-    free(pc.inv_diag); free(pc.blocks);
     return status;
 }
 

@@ -87,6 +87,21 @@ enum { ORC_OK = 0, ORC_ENOCONV = 2, ORC_EBREAKDOWN = 3, ORC_EINVAL = 1 };
 int orc_cg_solve(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, double tol,
                  int max_iterations, int precond, double *x, int *iterations, double *relres);
 
+/* cg_solve (linalg.cpp:292-362) with a caller-supplied preconditioner
+ * z = M^-1 r (fixed, SPD): the same control flow as orc_cg_solve. Used by
+ * the FP64 two-level Schwarz oracle (oracle/schwarz64.py), which gives the
+ * configs 3/4 an independent CPU solution in minutes instead of the
+ * ~21k Jacobi iterations the reference's own preconditioner needs. */
+typedef void (*orc_pc_fn)(void *ctx, const double *r, double *z);
+int orc_cg_solve_pc(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, double tol,
+                    int max_iterations, orc_pc_fn pc, void *pc_ctx, int exact_residual, double *x,
+                    int *iterations, double *relres);
+
+/* r = b - A_lifted x with long-double products and sums, rounded once
+ * (the true-residual check of orc_cg_solve_pc when exact_residual != 0). */
+void orc_residual_ld(const orc_system *s, uint32_t rows, uint32_t cols, const double *b, const double *x,
+                     double *r);
+
 /* Per-block recovery: gather_cell_values (global_stage.cpp:207-213) +
  * reconstruct_block_field (:215-230, sequential i) + evaluate_stress_in_element
  * (fem.cpp:262-301) + von_mises (:311-316) at 8 Gauss points (points = 8,

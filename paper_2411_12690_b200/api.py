@@ -213,6 +213,14 @@ class GpuGlobalStage:
                                            float(layout.pitch), float(layout.height)), "set_layout")
         self.layout = layout
 
+    def set_delta_t(self, delta_t):
+        """New per-block temperature change only (1 or rows*cols entries);
+        keeps index, BCs and preconditioner (tsv_set_delta_t)."""
+        dt = np.ascontiguousarray(np.atleast_1d(np.asarray(delta_t, np.float64)))
+        self._check(self._L.tsv_set_delta_t(self._h, _p(dt), dt.size), "set_delta_t")
+        if getattr(self, "layout", None) is not None:
+            self.layout.delta_t = dt
+
     def set_bc(self, kind: str = "bottom_pin_321"):
         self._check(self._L.tsv_set_bc(self._h, BC[kind]), "set_bc")
 

@@ -209,6 +209,7 @@ struct tsv_ctx {
     std::vector<uint32_t> dofmap;  // [B][n]
     size_t n = 0, ldk = 0, B = 0, B_pad = 0, m_tiles = 0, nodes = 0, N = 0;
     std::vector<int> row_cell, cell_row;
+    std::vector<double> dt_host;  // per panel row dT (set_delta_t staging)
     std::vector<uint8_t> row_kind, tile_kind;
     std::vector<double> row_dt;
     std::vector<uint32_t> node_glob_of_int, node_int_of_glob;
@@ -241,7 +242,7 @@ struct tsv_ctx {
     bool k1_streamk = false;  // large arrays: stream-K balanced K1
     // two-level additive Schwarz (precond 3)
     struct As2 {
-        int s = 0, SX = 0, SY = 0, Nc = 0, ncells = 0, ntypes = 0, step = 0;
+        int s = 0, SX = 0, SY = 0, Nc = 0, ncells = 0, ntypes = 0, step = 0, step_y = 0;
         size_t BL_pad = 0, mtiles = 0;
         DevBuf<int> slots2, tile_type, cell_ptr;
         DevBuf<double> XL, ZL, z, cellpart, rc, zc, ainv_c, ainv_store;
@@ -534,6 +535,25 @@ struct tsv_ctx {
         return v && *v && *v != '0';
     }
 
+    // Online dT update (ArrayLayout::delta_t, global.hpp:16-32): the
+    // thermal load is the only input that changes per call in the reference's
+    // online stage. Index, dof map, slots, masks, BCs and the preconditioner
+    // (a function of kinds and BCs only) stay; the RHS is re-assembled on the
+    // device on next use and recovery reads the new per-row dT.
+    void set_delta_t(const double *dt, size_t ndt) {
+        PhaseTimer pt("set_delta_t");
+        if (!layout_set) throw StatusError(TSV_ESTATE, "set_delta_t: no layout set");
+        if (!dt && ndt) throw StatusError(TSV_EINVAL, "layout: delta_t pointer is NULL");
+        if (ndt != 1 && ndt != B) throw StatusError(TSV_EINVAL, "layout: delta_t must have one entry or rows*cols entries");
+        layout.delta_t.assign(dt, dt + ndt);
+        dt_host.resize(B_pad);
+        for (size_t j = 0; j < B_pad; ++j) dt_host[j] = row_cell[j] >= 0 ? layout.delta_t_at(row_cell[j]) : 0.0;
+        row_dt_d.upload(dt_host.data(), dt_host.size(), stream);
+        rhs_dirty = true;
+        solution_valid = false;
+        CK(cudaStreamSynchronize(stream));  // dt_host is reused by the next call
+    }
+
     // ------------------------------------------------------------------ BC
     // mask: constrained DoFs (reference numbering); vals: the prescribed
     // (dof, value) pairs, sorted (only the non-zero values matter for lifting).
@@ -761,7 +781,9 @@ struct tsv_ctx {
         CK(cudaMemsetAsync(cinfo.ptr, 0, 2 * sizeof(int), stream));
         // --- 1. coarse space (first: its dense inverse runs on the device while
         // the host builds the local stage): corners of s x s super-blocks, bottom/top planes
-        const uint32_t q = nl.n_x;
+        // per-axis lattice steps: x uses n_x, y uses n_y, z uses n_z
+        // (NodeLayout axes, config.cpp:293-295; lat_y = rows*(n_y-1)+1)
+        const uint32_t q = nl.n_x, qy = nl.n_y, qz = nl.n_z;
         const int sb = schwarz_super_block(rows, cols);
         if (node_super_ptr.size() != static_cast<size_t>(((cols + sb - 1) / sb) * ((rows + sb - 1) / sb)) + 1)
             throw StatusError(TSV_ESTATE, "schwarz2: super-block size changed since set_layout");
@@ -769,6 +791,7 @@ struct tsv_ctx {
         as2.SX = static_cast<int>((cols + sb - 1) / sb);
         as2.SY = static_cast<int>((rows + sb - 1) / sb);
         as2.step = sb * static_cast<int>(q - 1);
+        as2.step_y = sb * static_cast<int>(qy - 1);
         as2.Nc = (as2.SX + 1) * (as2.SY + 1) * 6;
         as2.ncells = as2.SX * as2.SY;
         std::vector<short4> lat(nodes);
@@ -783,9 +806,9 @@ struct tsv_ctx {
             std::vector<double4> ct(static_cast<size_t>(as2.ncells));
             for (int c = 0; c < as2.ncells; ++c) {
                 for (int v = node_super_ptr[c]; v < node_super_ptr[c + 1]; ++v) nc[v] = c;
-                const int x0 = (c % as2.SX) * as2.step, y0 = (c / as2.SX) * as2.step;
+                const int x0 = (c % as2.SX) * as2.step, y0 = (c / as2.SX) * as2.step_y;
                 const int x1 = std::min<int>(x0 + as2.step, static_cast<int>(index.lat_x) - 1);
-                const int y1 = std::min<int>(y0 + as2.step, static_cast<int>(index.lat_y) - 1);
+                const int y1 = std::min<int>(y0 + as2.step_y, static_cast<int>(index.lat_y) - 1);
                 ct[c] = make_double4(x0, y0, 1.0 / static_cast<double>(x1 - x0), 1.0 / static_cast<double>(y1 - y0));
             }
             as2.node_cell.upload(nc.data(), nc.size(), stream);
@@ -813,9 +836,9 @@ struct tsv_ctx {
                 const size_t cell = static_cast<size_t>(r) * cols + c;
                 const uint32_t *dm = dofmap.data() + cell * n;
                 const int cx = static_cast<int>(c) / sb, cy = static_cast<int>(r) / sb;
-                const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step;
-                const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step, index.lat_y - 1);
-                const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (q - 1);
+                const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step_y;
+                const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step_y, index.lat_y - 1);
+                const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (qy - 1);
                 std::vector<long> &key = keys[cell];
                 key = {layout.kind_at(cell), bx - x0, x1 - x0, by - y0, y1 - y0};
                 for (size_t a = 0; a < n; ++a)
@@ -827,9 +850,9 @@ struct tsv_ctx {
                 const size_t cell = static_cast<size_t>(r) * cols + c;
                 const uint32_t *dm = dofmap.data() + cell * n;
                 const int cx = static_cast<int>(c) / sb, cy = static_cast<int>(r) / sb;
-                const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step;
-                const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step, index.lat_y - 1);
-                const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (q - 1);
+                const long x0 = static_cast<long>(cx) * as2.step, y0 = static_cast<long>(cy) * as2.step_y;
+                const long x1 = std::min<long>(x0 + as2.step, index.lat_x - 1), y1 = std::min<long>(y0 + as2.step_y, index.lat_y - 1);
+                const long bx = static_cast<long>(c) * (q - 1), by = static_cast<long>(r) * (qy - 1);
                 const std::vector<long> &key = keys[cell];
                 auto it = key_id.find(key);
                 if (it == key_id.end()) {
@@ -843,7 +866,7 @@ struct tsv_ctx {
                     for (size_t rank = 0; rank < nn; ++rank) {
                         const double tx = static_cast<double>(bx + snodes[rank][0] - x0) / static_cast<double>(x1 - x0);
                         const double ty = static_cast<double>(by + snodes[rank][1] - y0) / static_cast<double>(y1 - y0);
-                        const double tz = static_cast<double>(snodes[rank][2]) / static_cast<double>(q - 1);
+                        const double tz = static_cast<double>(snodes[rank][2]) / static_cast<double>(qz - 1);
                         for (int k = 0; k < 8; ++k) {
                             const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
                             for (int comp = 0; comp < 3; ++comp) {
@@ -1223,13 +1246,11 @@ struct tsv_ctx {
         };
         make(&as2.tmA, as2.XL32.ptr, as2.BL_pad, static_cast<uint32_t>(kTcBM), as2.LD);
         make(&as2.tmB, as2.ainv32.ptr, static_cast<uint64_t>(T) * as2.NP, static_cast<uint32_t>(as2.BN), as2.KP);
-        static bool attr = false;
-        if (!attr) {
-            CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
-            CK(cudaFuncSetAttribute(tc_local_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    tc_pair_smem_bytes(256)));
-            attr = true;
-        }
+        // per-device function attributes: set on this context's device every
+        // build (a process-wide flag would skip a second device)
+        CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
+        CK(cudaFuncSetAttribute(tc_local_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tc_pair_smem_bytes(256)));
     }
 
     void launch_tc_local() {
@@ -1263,6 +1284,7 @@ struct tsv_ctx {
         a.z = as2.z.ptr;
         a.lat = as2.lat.ptr;
         a.step = as2.step;
+        a.step_y = as2.step_y;
         a.SX = as2.SX;
         a.SY = as2.SY;
         a.lat_x = static_cast<int>(index.lat_x);
@@ -1441,11 +1463,7 @@ struct tsv_ctx {
             const RomHost &m = rom[k].set ? rom[k] : rom[1 - k];
             make(&oz_tmB[k], m.oz_b.ptr, static_cast<uint64_t>(S) * oz_brows, static_cast<uint32_t>(BN));
         }
-        static bool attr[2] = {false, false};
-        if (!attr[S - 9]) {
-            CK(cudaFuncSetAttribute(oz_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes<S>()));
-            attr[S - 9] = true;
-        }
+        CK(cudaFuncSetAttribute(oz_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, oz_smem_bytes<S>()));
         oz_s = S;
     }
 
@@ -1602,7 +1620,12 @@ struct tsv_ctx {
             status = TSV_ENOCONV;
             best_it = st.best_it;
             relres = st.best_res / st.norm_b;
-            if (st.best_it < st.it) {
+            if (st.best_it == 0) {
+                // no iterate beat the initial residual: the reference returns
+                // best_x = x0 = 0 (linalg.cpp:316-317, 354-355); a replay
+                // would still run one update (max_it is checked after it += 1)
+                CK(cudaMemsetAsync(x.ptr, 0, x.count * sizeof(double), stream));
+            } else if (st.best_it < st.it) {
                 // Bitwise-deterministic replay up to the best iterate
                 // (the reference keeps a copy of it, linalg.cpp:346-349).
                 CgState st2 = run_cg(o.tolerance, st.best_it);
@@ -2224,6 +2247,14 @@ int tsv_set_layout(tsv_ctx *ctx, uint32_t rows, uint32_t cols, const uint8_t *ki
     return guarded(ctx, [&] {
         cudaSetDevice(ctx->device);
         ctx->build_layout(rows, cols, kinds, delta_t, n_delta_t, pitch, height);
+        return TSV_OK;
+    });
+}
+
+int tsv_set_delta_t(tsv_ctx *ctx, const double *delta_t, size_t n_delta_t) {
+    return guarded(ctx, [&] {
+        cudaSetDevice(ctx->device);
+        ctx->set_delta_t(delta_t, n_delta_t);
         return TSV_OK;
     });
 }

@@ -31,7 +31,7 @@ struct AsParams {
     const float *ZL32;     // local-solve product panel (tensor-core path)
     double *z;             // [3][node] preconditioned residual
     const short4 *lat;     // (gx, gy, gz) lattice position of each internal node
-    int step, SX, SY, lat_x, lat_y, qm1;
+    int step, step_y, SX, SY, lat_x, lat_y, qm1;  // super-cell steps along x / y (lattice units)
     const int *cell_ptr;   // super cell -> its contiguous internal node range
     const int *node_cell;  // internal node -> its super cell
     const double4 *celltab;  // per super cell: x0, y0, 1/dx, 1/dy (lattice units)
@@ -85,9 +85,9 @@ __device__ __forceinline__ AsCell as_cell(const AsParams &a, int cell) {
     c.cx = cell % a.SX;
     c.cy = cell / a.SX;
     c.x0 = c.cx * a.step;
-    c.y0 = c.cy * a.step;
+    c.y0 = c.cy * a.step_y;
     c.rdx = 1.0 / static_cast<double>(min(c.x0 + a.step, a.lat_x - 1) - c.x0);
-    c.rdy = 1.0 / static_cast<double>(min(c.y0 + a.step, a.lat_y - 1) - c.y0);
+    c.rdy = 1.0 / static_cast<double>(min(c.y0 + a.step_y, a.lat_y - 1) - c.y0);
     c.rdz = 1.0 / static_cast<double>(a.qm1);
     return c;
 }

@@ -15,7 +15,7 @@ TSV_OK, TSV_EINVAL, TSV_ENOCONV, TSV_EBREAKDOWN, TSV_ECUDA, TSV_ENOMEM, TSV_ESTA
 
 # Every symbol include/tsv_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "tsv_ctx_create", "tsv_ctx_destroy", "tsv_last_error", "tsv_abi_version", "tsv_set_rom", "tsv_set_layout",
+    "tsv_ctx_create", "tsv_ctx_destroy", "tsv_last_error", "tsv_abi_version", "tsv_set_rom", "tsv_set_layout", "tsv_set_delta_t",
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
     "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_precond_apply", "tsv_precond_setup", "tsv_debug_coarse", "tsv_solve", "tsv_set_solution", "tsv_recover",
     "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
@@ -92,6 +92,7 @@ def load(path: str = LIB_PATH):
         "tsv_abi_version": (i, []),
         "tsv_set_rom": (i, [vp, i, P(RomDesc)]),
         "tsv_set_layout": (i, [vp, u32, u32, vp, vp, sz, d, d]),
+        "tsv_set_delta_t": (i, [vp, vp, sz]),
         "tsv_set_dirichlet": (i, [vp, sz, vp, vp]),
         "tsv_set_bc": (i, [vp, i]),
         "tsv_index_global_nodes": (i, [u32, u32, vp, P(u64), vp, vp, vp, vp]),
