@@ -3,7 +3,7 @@
 
 ROMs (the local-stage output, an INPUT of the hot path) come from the
 reference's own build_rom (oracle/_ref, compiled from the unmodified
-sources) and are cached under .cache/roms/ in the reference's MRST format.
+sources) and are cached under ~/.cache/tsv_b200_roms/ in the reference's MRST format.
 """
 from __future__ import annotations
 
@@ -16,7 +16,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-CACHE = os.path.join(ROOT, ".cache", "roms")
+CACHE = os.environ.get("TSV_ROM_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "tsv_b200_roms"))  # outside the repo: not shipped to the GPU box
 
 
 def pytest_configure(config):
