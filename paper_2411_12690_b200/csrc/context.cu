@@ -264,6 +264,12 @@ struct tsv_ctx {
         DevBuf<float> sym_tiles;
         DevBuf<double> sym_part, dotpart, kcell_d, cwork;
         int sym_nt = 0;
+        // split loop: A P zc panel and its per-key products
+        DevBuf<double> Yc, kp;
+        DevBuf<int4> kp_items;
+        DevBuf<int> kp_rows;
+        int kp_nitems = 0;
+        size_t kp_smem = 0;
     } as2;
     // int8 (Ozaki) K1: digit planes of the X panel
     int oz_s = 0;            // digits per value (0 = DMMA K1)
@@ -881,7 +887,7 @@ struct tsv_ctx {
         const int nkeys = static_cast<int>(key_kind.size());
         tick("coarse keys");
         if (dbg) std::fprintf(stderr, "[schwarz2] keys %d s %d Nc %d n %zu\n", nkeys, sb, as2.Nc, n);
-        std::vector<double> Kcall[2];
+        std::vector<double> Kcall[2], KPall[2];
         {
             DevBuf<double> dP, dKP, dKc, dK;
             const double one = 1.0, zero = 0.0;
@@ -901,9 +907,49 @@ struct tsv_ctx {
                     throw StatusError(TSV_ECUDA, "schwarz2: coarse Galerkin products failed");
                 Kcall[kind].resize(static_cast<size_t>(cnt) * 576);
                 d2h(Kcall[kind].data(), dKc.ptr, Kcall[kind].size() * sizeof(double), stream);
+                KPall[kind].resize(Pall[kind].size());
+                d2h(KPall[kind].data(), dKP.ptr, KPall[kind].size() * sizeof(double), stream);
             }
         }
         tick("coarse products (device)");
+        {
+            // split loop: K_b P_b per key in the internal panel row order
+            // (c nn + rank) x 24, and the panel rows grouped by key in chunks
+            const size_t nnl = n / 3;
+            std::vector<double> kph(static_cast<size_t>(nkeys) * ldk * 24, 0.0);
+            for (int key = 0; key < nkeys; ++key) {
+                const double *src = KPall[key_kind[key]].data() + static_cast<size_t>(key_local[key]) * n * 24;
+                double *dst = kph.data() + static_cast<size_t>(key) * ldk * 24;
+                for (size_t ai = 0; ai < n; ++ai) {
+                    const size_t a_ref = 3 * (ai % nnl) + ai / nnl;
+                    for (int j = 0; j < 24; ++j) dst[ai * 24 + j] = src[static_cast<size_t>(j) * n + a_ref];
+                }
+            }
+            as2.kp.upload(kph.data(), kph.size(), stream);
+            std::vector<std::vector<int>> rows_of(static_cast<size_t>(nkeys));
+            for (size_t j = 0; j < B_pad; ++j)
+                if (row_cell[j] >= 0) rows_of[static_cast<size_t>(key_of[static_cast<size_t>(row_cell[j])])].push_back(static_cast<int>(j));
+            std::vector<int> krows;
+            std::vector<int4> items;
+            for (int key = 0; key < nkeys; ++key) {
+                const auto &v = rows_of[static_cast<size_t>(key)];
+                for (size_t i0 = 0; i0 < v.size(); i0 += kKpzcChunk) {
+                    const int b0 = static_cast<int>(krows.size() + i0);
+                    const int b1 = static_cast<int>(krows.size() + std::min(v.size(), i0 + kKpzcChunk));
+                    items.push_back(make_int4(key, b0, b1, 0));
+                }
+                krows.insert(krows.end(), v.begin(), v.end());
+            }
+            as2.kp_rows.upload(krows.data(), krows.size(), stream);
+            as2.kp_items.upload(items.data(), items.size(), stream);
+            as2.kp_nitems = static_cast<int>(items.size());
+            as2.kp_smem = (n * kpzc_ld() + static_cast<size_t>(kKpzcChunk) * 24) * sizeof(double);
+            if (as2.kp_smem > 227 * 1024) throw StatusError(TSV_EINVAL, "schwarz2: per-key coarse product too large for shared memory");
+            CK(cudaFuncSetAttribute(as_kpzc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(as2.kp_smem)));
+            as2.Yc.alloc(B_pad * ldk);
+            CK(cudaMemsetAsync(as2.Yc.ptr, 0, B_pad * ldk * sizeof(double), stream));
+            CK(cudaStreamSynchronize(stream));  // host staging vectors go out of scope
+        }
         // per super cell: sum of its blocks' products in block order
         std::vector<double> kcell(static_cast<size_t>(as2.ncells) * 576, 0.0);
         for (uint32_t r = 0; r < rows; ++r)
@@ -1285,6 +1331,7 @@ struct tsv_ctx {
         a.lat = as2.lat.ptr;
         a.step = as2.step;
         a.step_y = as2.step_y;
+        a.Yc = as2.Yc.ptr;
         a.SX = as2.SX;
         a.SY = as2.SY;
         a.lat_x = static_cast<int>(index.lat_x);
@@ -1312,12 +1359,19 @@ struct tsv_ctx {
 
     // r update + two-level Schwarz z = M r (U', local GEMM, restriction,
     // coarse solve, prolongation + r.z).
-    void launch_as_update_precond(const CgParams &q) {
+    void launch_as_update_precond(const CgParams &q, bool with_gather) {
         AsParams a = as_params();
         // r update (grid-stride). Fusing the coarse restriction in (warp-level
         // per-cell partials) measured slower at config 3: 80 us vs 47 + 34 us
         // with the restriction off the critical path on the side stream.
-        launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+        if (!with_gather) {
+            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+        } else if (fused_gu()) {
+            launch_pdl(as_gather_update_kernel, gu_grid(), kVecThreads, 0, stream, q, a);
+        } else {
+            launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
+            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+        }
         // fork: the coarse chain (cell sums of the restriction -> coarse rhs
         // -> coarse solve, HBM and latency bound) runs on a side stream beside
         // the local solves (tensor cores); both join before z. Captured as a
@@ -1565,11 +1619,17 @@ struct tsv_ctx {
     }
 
     void launch_iteration(const CgParams &q) {
+        if (pre_kind == TSV_PRECOND_SCHWARZ2 && as_split()) {
+            launch_pdl(as_gu_split_kernel, gu_split_grid(), kVecThreads, 0, stream, q, as_params());
+            ++launches;
+            launch_split_tail(q);
+            return;
+        }
         launch_k1(&state.ptr->done);
-        launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
         if (pre_kind == TSV_PRECOND_SCHWARZ2) {
-            launch_as_update_precond(q);
+            launch_as_update_precond(q, true);
         } else {
+            launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
             launch_pdl(cg_update_kernel, cg_grid(), kVecThreads, 0, stream, q);
             ++launches;
         }
@@ -1578,8 +1638,88 @@ struct tsv_ctx {
     }
 
     int graph_kernels_per_iteration() const {
-        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? 10 : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
+        const int schwarz = as_split() ? 10 : (fused_gu() ? 9 : 10);
+        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? schwarz : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
     }
+
+    // Split Schwarz loop (default; TSV_AS_SPLIT=0 restores the serial one):
+    // after r is updated, the coarse chain runs on the side stream beside the
+    // local solve, z_l and K1 (A z_l); A P zc enters through the Yc panel.
+    static bool as_split() {
+        const char *v = getenv("TSV_AS_SPLIT");
+        return !(v && *v == '0');
+    }
+    unsigned gu_split_grid() {
+        if (!gu_split_grid_) {
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, as_gu_split_kernel, kVecThreads, 0));
+            if (per_sm < 1) throw StatusError(TSV_ECUDA, "as_gu_split_kernel: no resident CTA");
+            gu_split_grid_ = static_cast<unsigned>(per_sm * sm_count);
+        }
+        return std::min<unsigned>(vec_grid(), gu_split_grid_);
+    }
+    unsigned gu_split_grid_ = 0;
+
+    KpzcParams kpzc_params() const {
+        KpzcParams k{};
+        k.kp = as2.kp.ptr;
+        k.items = as2.kp_items.ptr;
+        k.rows = as2.kp_rows.ptr;
+        k.row_cell = row_cell_d.ptr;
+        k.cols = static_cast<int>(layout.cols);
+        k.sb = as2.s;
+        k.n = static_cast<int>(n);
+        k.ldk = static_cast<long long>(ldk);
+        return k;
+    }
+
+    // After r is updated (prologue U or GU): fork the coarse chain (+ A P zc)
+    // to the side stream; local solve, z_l / X panel and K1 on the main
+    // stream; join.
+    void launch_split_tail(const CgParams &q) {
+        AsParams a = as_params();
+        CK(cudaEventRecord(ev_fork, stream));
+        CK(cudaStreamWaitEvent(side, ev_fork, 0));
+        launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 3 * kRestrictGroup, 0, side, q, a);
+        launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, side, q, a);
+        if (as2.sym_nt) {
+            const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
+            launch_pdl(as_coarse_symv_kernel, ntiles, 128, 0, side, q, a, static_cast<const float *>(as2.sym_tiles.ptr),
+                       as2.sym_nt, as2.sym_part.ptr);
+            launch_pdl(as_coarse_symv_reduce_kernel, as2.sym_nt, kSymRedG * kSymT, 0, side, q, a, as2.sym_nt,
+                       static_cast<const double *>(as2.sym_part.ptr));
+        } else {
+            as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
+            as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
+        }
+        launch_pdl(as_kpzc_kernel, static_cast<unsigned>(as2.kp_nitems), 256, as2.kp_smem, side, q, a, kpzc_params());
+        CK(cudaEventRecord(ev_join, side));
+        if (as2.tc) {
+            launch_tc_local();
+        } else {
+            GemmParams gp = local_gemm_params();
+            gemm_nt_f64<K1SmallCfg><<<std::min(k1s_grid, gp.m_tiles * gp.n_tiles), K1SmallCfg::THREADS, K1SmallCfg::SMEM,
+                                      stream>>>(gp);
+        }
+        launch_pdl(as_zl_split_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+        launches += 7;
+        launch_k1(&state.ptr->done);
+        CK(cudaStreamWaitEvent(stream, ev_join, 0));
+    }
+
+    // Gather + update as one kernel across a software grid barrier (Schwarz
+    // path; TSV_NO_FUSED_GU=1 keeps the two kernels).
+    static bool fused_gu() { return !getenv_flag("TSV_NO_FUSED_GU"); }
+    unsigned gu_grid() {
+        if (!gu_grid_) {
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, as_gather_update_kernel, kVecThreads, 0));
+            if (per_sm < 1) throw StatusError(TSV_ECUDA, "as_gather_update_kernel: no resident CTA");
+            gu_grid_ = static_cast<unsigned>(per_sm * sm_count);
+        }
+        return std::min<unsigned>(vec_grid(), gu_grid_);
+    }
+    unsigned gu_grid_ = 0;
 
     void ensure_graph() {
         oz_ensure();
@@ -1680,13 +1820,19 @@ struct tsv_ctx {
         CK(cudaMemcpyAsync(state.ptr, h_state, sizeof(CgState), cudaMemcpyHostToDevice, stream));
         CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), stream));
         CgParams q = cg_params();
-        if (pre_kind == TSV_PRECOND_SCHWARZ2) {
-            launch_as_update_precond(q);
-        } else {
-            cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+        if (pre_kind == TSV_PRECOND_SCHWARZ2 && as_split()) {
+            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, as_params());
             ++launches;
+            launch_split_tail(q);
+        } else {
+            if (pre_kind == TSV_PRECOND_SCHWARZ2) {
+                launch_as_update_precond(q, false);
+            } else {
+                cg_update_kernel<<<cg_grid(), kVecThreads, 0, stream>>>(q);
+                ++launches;
+            }
+            launch_scatter_p(q);
         }
-        launch_scatter_p(q);
         CK(cudaGetLastError());
         // Host-polled batches of graph-captured iterations; a finished
         // solve turns the remaining launches into early exits.
@@ -2386,7 +2532,7 @@ int tsv_precond_apply(tsv_ctx *ctx, int precond, const double *r_in, double *z_o
         *ctx->h_state = st;
         CK(cudaMemcpyAsync(ctx->state.ptr, ctx->h_state, sizeof(CgState), cudaMemcpyHostToDevice, ctx->stream));
         CgParams q = ctx->cg_params();
-        ctx->launch_as_update_precond(q);
+        ctx->launch_as_update_precond(q, false);
         ctx->launch_scatter_p(q, 1);  // z = z_l + P zc (p / panel updates are discarded)
         CK(cudaGetLastError());
         std::vector<double> zi(ctx->N);

@@ -348,10 +348,12 @@ struct CgState {
     int y_holds_x;  // 1: the next product is A x (true-residual verification)
     int phase;      // what the B kernel does this iteration
     int p_assign;   // 1: p = z (fresh start), 0: p = z + beta p
+    int fresh;      // split Schwarz loop: the next p is z (after init / restart)
     int it, best_it, max_it, breakdown_code, restarts;
     double rho, alpha, beta, res, best_res, norm_b, tol, tol_abs;
     double rz_l, rz_c;  // Schwarz: r.z split into the local part and (P^T r).zc
     unsigned ticket_a, ticket_b, ticket_c;  // c: side-stream kernels
+    unsigned bar_gen;                       // software grid barrier generation (fused kernels)
 };
 
 // Device vectors are structure-of-arrays per component: DoF (node, c) of
@@ -450,14 +452,11 @@ __device__ __forceinline__ bool publish_partials(const double (&v)[NV], double *
 
 // A: Y (= A p or A x) summed per owned DoF; p'Ap or the true residual.
 // Grid-stride over nodes with a fixed grid (deterministic reduction).
-__global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
-    pdl_wait();
-    __shared__ double sh[64];
-    CgState *st = q.st;
-    if (*reinterpret_cast<volatile int *>(&st->done)) return;
-    const int yx = st->y_holds_x;
+// Node loop of the gather (A): Ap = sum over the node's block copies of Y
+// (unit rows on constrained DoFs), p.Ap; or, verifying, r = b - A x, r.r.
+__device__ __forceinline__ double cg_gather_nodes(const CgParams &q, int yx) {
     const int N = q.n_nodes;
-    double part[1] = {0.0};
+    double part = 0.0;
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
 #pragma unroll
@@ -476,14 +475,47 @@ __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
             }
             if (!yx) {
                 q.ap[dof] = acc;
-                part[0] += q.p[dof] * acc;
+                part += q.p[dof] * acc;
             } else {
                 const double rt = q.b[dof] - acc;
                 q.r[dof] = rt;
-                part[0] += rt * rt;
+                part += rt * rt;
             }
         }
     }
+    return part;
+}
+
+// Loop bookkeeping after the gather's reduction (one thread): alpha, or the
+// verification verdict (converged / restart), linalg.cpp:321-336.
+__device__ __forceinline__ void cg_gather_finish(CgState *st, int yx, double tot) {
+    if (!yx) {
+        const double pap = tot;
+        if (!isfinite(pap)) {
+            st->done = CG_BREAKDOWN;
+            st->breakdown_code = 1;  // NaN/Inf
+        } else if (pap <= 0.0) {
+            st->done = CG_BREAKDOWN;
+            st->breakdown_code = 2;  // p'Ap <= 0
+        } else {
+            st->alpha = st->rho / pap;
+        }
+        st->phase = PH_NORMAL;
+    } else {
+        st->res = sqrt(tot);
+        if (st->res <= st->tol_abs) st->done = CG_CONVERGED;
+        else st->restarts += 1;
+        st->phase = PH_RESTART;
+    }
+}
+
+__global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
+    pdl_wait();
+    __shared__ double sh[64];
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int yx = st->y_holds_x;
+    double part[1] = {cg_gather_nodes(q, yx)};
     pdl_trigger();
     block_sum<1>(part, sh);
     if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
@@ -491,24 +523,7 @@ __global__ void __launch_bounds__(256) cg_gather_kernel(CgParams q) {
     grid_sum<1>(q.partial, gridDim.x, tot, sh);
     if (threadIdx.x == 0) {
         st->ticket_a = 0u;
-        if (!yx) {
-            const double pap = tot[0];
-            if (!isfinite(pap)) {
-                st->done = CG_BREAKDOWN;
-                st->breakdown_code = 1;  // NaN/Inf
-            } else if (pap <= 0.0) {
-                st->done = CG_BREAKDOWN;
-                st->breakdown_code = 2;  // p'Ap <= 0
-            } else {
-                st->alpha = st->rho / pap;
-            }
-            st->phase = PH_NORMAL;
-        } else {
-            st->res = sqrt(tot[0]);
-            if (st->res <= st->tol_abs) st->done = CG_CONVERGED;
-            else st->restarts += 1;
-            st->phase = PH_RESTART;
-        }
+        cg_gather_finish(st, yx, tot[0]);
         __threadfence();
     }
 }

@@ -49,7 +49,24 @@ struct AsParams {
     // tensor-core local solve (tc_local.cuh): TF32 operand panel (same
     // row stride as ZL, so slots2 addresses both)
     float *XL32;
+    // split loop: A P zc as a block panel (same layout as Y), from the
+    // per-key products K_b P_b (as_kpzc_kernel)
+    double *Yc;
 };
+
+// as_kpzc_kernel work: per-key K_b P_b ([key][ldk][24], internal row order
+// c nn + rank, columns 3 corner + comp), panel rows sorted by key, and
+// (key, begin, end) items over that list.
+struct KpzcParams {
+    const double *kp;
+    const int4 *items;
+    const int *rows;
+    const int *row_cell;
+    int cols, sb, n;
+    long long ldk;
+};
+constexpr int kKpzcChunk = 64;
+__host__ __device__ constexpr int kpzc_ld() { return 25; }  // odd-word row stride: conflict-free 8 B smem reads
 
 // Round to `bits` explicit mantissa bits (emulates a low-precision operand).
 __device__ __forceinline__ double round_mantissa(double v, int bits) {
@@ -114,15 +131,10 @@ __device__ __forceinline__ int as_corner_node(const AsParams &a, int cx, int cy,
 // the loop-head bookkeeping of cg_solve (iteration count, best iterate,
 // max-iteration exit, next product = A x when the residual test passes).
 
-__global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) {
-    pdl_wait();
-    __shared__ double sh[64];
-    CgState *st = q.st;
-    if (*reinterpret_cast<volatile int *>(&st->done)) return;
-    const int phase = st->phase;
-    const double alpha = st->alpha;
+// Node loop of U' (grid-stride): returns this thread's r.r partial.
+__device__ __forceinline__ double as_update_nodes(const CgParams &q, const AsParams &a, int phase, double alpha) {
     const int N = q.n_nodes;
-    double part[1] = {0.0};
+    double part = 0.0;
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
 #pragma unroll
@@ -140,7 +152,7 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             } else {
                 rv = q.r[dof];
             }
-            part[0] += rv * rv;
+            part += rv * rv;
             if (q.cmask[dof]) continue;
             const int co = c * q.nn;
             if (a.XL32) {
@@ -158,15 +170,16 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             }
         }
     }
-    pdl_trigger();
-    block_sum<1>(part, sh);
-    if (!publish_partials<1>(part, q.partial, &st->ticket_b)) return;
-    double tot[1];
-    grid_sum<1>(q.partial, gridDim.x, tot, sh);
-    if (threadIdx.x != 0) return;
-    st->ticket_b = 0u;
+    return part;
+}
+
+// Loop-head bookkeeping of cg_solve after r.r (one thread): iteration count,
+// best iterate, max-iteration exit, next product = A x when the residual
+// test passes (linalg.cpp:310-350).
+__device__ __forceinline__ void as_update_finish(CgState *st, int phase, double tot) {
+    if (phase != PH_NORMAL) st->fresh = 1;  // split loop: p = z next
     if (phase == PH_INIT) {
-        st->norm_b = sqrt(tot[0]);
+        st->norm_b = sqrt(tot);
         st->tol_abs = st->tol * st->norm_b;
         st->res = st->norm_b;
         st->best_res = st->res;
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
     } else if (phase == PH_RESTART) {
         st->y_holds_x = 0;
     } else {
-        st->res = sqrt(tot[0]);
+        st->res = sqrt(tot);
         if (!isfinite(st->res)) {
             st->done = CG_BREAKDOWN;
             st->breakdown_code = 1;
@@ -200,6 +213,76 @@ __global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) 
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(256) as_update_kernel(CgParams q, AsParams a) {
+    pdl_wait();
+    __shared__ double sh[64];
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int phase = st->phase;
+    double part[1] = {as_update_nodes(q, a, phase, st->alpha)};
+    pdl_trigger();
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial, &st->ticket_b)) return;
+    double tot[1];
+    grid_sum<1>(q.partial, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_b = 0u;
+    as_update_finish(st, phase, tot[0]);
+    __threadfence();
+}
+
+// Gather (A) and update (U') fused across one software grid barrier: the
+// p.Ap reduction that alpha needs is finished by the last CTA to arrive,
+// which then releases the others (generation counter). Ap stays in L2
+// between the halves; one launch and one kernel boundary less per
+// iteration. The grid must be co-resident (host: occupancy x SMs), and
+// dependents are released only after the barrier (a PDL-launched successor
+// cannot take the slots of CTAs that have not arrived yet).
+__global__ void __launch_bounds__(256, 8) as_gather_update_kernel(CgParams q, AsParams a) {
+    pdl_wait();
+    __shared__ double sh[64];
+    __shared__ bool last;
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const unsigned gen = *reinterpret_cast<volatile unsigned *>(&st->bar_gen);
+    const int yx = st->y_holds_x;
+    double part[1] = {cg_gather_nodes(q, yx)};
+    block_sum<1>(part, sh);
+    if (threadIdx.x == 0) {
+        q.partial[blockIdx.x] = part[0];
+        __threadfence();
+        last = atomicAdd(&st->ticket_a, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double tot[1];
+        grid_sum<1>(q.partial, gridDim.x, tot, sh);
+        if (threadIdx.x == 0) {
+            st->ticket_a = 0u;
+            cg_gather_finish(st, yx, tot[0]);
+            __threadfence();
+            atomicExch(&st->bar_gen, gen + 1u);
+        }
+    } else if (threadIdx.x == 0) {
+        while (*reinterpret_cast<volatile unsigned *>(&st->bar_gen) == gen) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+    pdl_trigger();
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;  // breakdown or converged (verification)
+    const int phase = *reinterpret_cast<volatile int *>(&st->phase);
+    const double alpha = *reinterpret_cast<volatile double *>(&st->alpha);
+    part[0] = as_update_nodes(q, a, phase, alpha);
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial + gridDim.x, &st->ticket_b)) return;
+    double tot[1];
+    grid_sum<1>(q.partial + gridDim.x, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_b = 0u;
+    as_update_finish(st, phase, tot[0]);
     __threadfence();
 }
 
@@ -565,6 +648,215 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
         st->phase = PH_NORMAL;
     }
     st->rho = rz;
+    __threadfence();
+}
+
+// ------------------------------------------------------------------------
+// Split two-level Schwarz loop. With z = z_l + P zc, the next operator
+// product is formed as
+//     A p = A z_l + A P zc + beta A p_old,   p = z_l + P zc + beta p_old,
+// so K1 multiplies the local part z_l (ready right after the tensor-core
+// local solves) while the coarse chain (restriction, coarse solve, and
+// A P zc = sum_b G_b^T (K_b P_b) zc_b) runs beside it on the side stream
+// instead of in front of it. The reference's control flow is unchanged: the
+// same stopping test, true-residual verification (K1 on x) and restart.
+// Per iteration: GU (gather + p/Ap recurrences | grid barrier | x, r update)
+// -> {coarse chain} || {tc local solve -> z_l (+ X panel) -> K1} -> join.
+
+// z_l = sum of the node's local products (r on constrained DoFs), r.z_l,
+// and the next K1 operand: z_l (or x when verifying) into the X panel.
+__global__ void __launch_bounds__(256) as_zl_split_kernel(CgParams q, AsParams a) {
+    pdl_wait();
+    __shared__ double sh[64];
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int yx = st->y_holds_x;
+    const int N = q.n_nodes;
+    double part[1] = {0.0};
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+        const int4 s2 = reinterpret_cast<const int4 *>(a.slots2)[node];
+        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            const double rv = q.r[dof];
+            const bool cm = q.cmask[dof] != 0;
+            const int co = c * q.nn;
+            double zv;
+            if (cm) {
+                zv = rv;  // unit row of the lifted matrix
+            } else if (a.ZL32) {
+                zv = 0.0;
+                if (s2.x >= 0) zv += static_cast<double>(a.ZL32[s2.x + co]);
+                if (s2.y >= 0) zv += static_cast<double>(a.ZL32[s2.y + co]);
+                if (s2.z >= 0) zv += static_cast<double>(a.ZL32[s2.z + co]);
+                if (s2.w >= 0) zv += static_cast<double>(a.ZL32[s2.w + co]);
+            } else {
+                zv = 0.0;
+                if (s2.x >= 0) zv += a.ZL[s2.x + co];
+                if (s2.y >= 0) zv += a.ZL[s2.y + co];
+                if (s2.z >= 0) zv += a.ZL[s2.z + co];
+                if (s2.w >= 0) zv += a.ZL[s2.w + co];
+            }
+            a.z[dof] = zv;
+            part[0] += rv * zv;
+            if (cm) continue;
+            const double v = yx ? q.x[dof] : zv;
+            if (s.x >= 0) q.X[s.x + co] = v;
+            if (s.y >= 0) q.X[s.y + co] = v;
+            if (s.z >= 0) q.X[s.z + co] = v;
+            if (s.w >= 0) q.X[s.w + co] = v;
+        }
+    }
+    pdl_trigger();
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
+    double tot[1];
+    grid_sum<1>(q.partial, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_a = 0u;
+    st->rz_l = tot[0];
+    __threadfence();
+}
+
+// A P zc per block: Yc[row] = (K_b P_b) zc_cell(b), one CTA per (key, up
+// to kKpzcChunk blocks of that key); the key's n x 24 product sits in shared
+// memory. Side stream, after the coarse solve.
+__global__ void __launch_bounds__(256) as_kpzc_kernel(CgParams q, AsParams a, KpzcParams k) {
+    pdl_wait();
+    extern __shared__ double smk[];
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    const int4 it = k.items[blockIdx.x];
+    const int n = k.n, nb = it.z - it.y;
+    double *kps = smk;                                  // [n][kpzc_ld()]
+    double *zcs = smk + static_cast<size_t>(n) * kpzc_ld();  // [kKpzcChunk][24]
+    const double *kp = k.kp + static_cast<long long>(it.x) * k.ldk * 24;
+    for (int i = threadIdx.x; i < n * 24; i += blockDim.x) kps[(i / 24) * kpzc_ld() + i % 24] = __ldg(kp + i);
+    for (int i = threadIdx.x; i < nb * 24; i += blockDim.x) {
+        const int bi = i / 24, j = i % 24;
+        const int cell = k.row_cell[k.rows[it.y + bi]];
+        const int cx = (cell % k.cols) / k.sb, cy = (cell / k.cols) / k.sb;
+        zcs[i] = a.zc[3 * as_corner_node(a, cx, cy, j / 3) + j % 3];
+    }
+    __syncthreads();
+    pdl_trigger();
+    for (int bi = 0; bi < nb; ++bi) {
+        double *yrow = a.Yc + static_cast<long long>(k.rows[it.y + bi]) * k.ldk;
+        const double *zb = zcs + bi * 24;
+        for (int r = threadIdx.x; r < n; r += blockDim.x) {
+            const double *kr = kps + r * kpzc_ld();
+            double y = 0.0;
+#pragma unroll
+            for (int j = 0; j < 24; ++j) y += kr[j] * zb[j];
+            yrow[r] = y;
+        }
+    }
+}
+
+// Node loop of GU's first half: p = z_l + P zc + beta p, A p = sum(Y) +
+// sum(Yc) + beta A p (unit rows on constrained DoFs), returns p.Ap; or,
+// verifying, r = b - A x, returns r.r.
+__device__ __forceinline__ double as_gu_nodes(const CgParams &q, const AsParams &a, int yx, bool fresh, double beta) {
+    if (yx) return cg_gather_nodes(q, 1);
+    const int N = q.n_nodes;
+    const double rdz = 1.0 / static_cast<double>(a.qm1);
+    double part = 0.0;
+    for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
+        const int cell = a.node_cell[node];
+        const double4 ct = a.celltab[cell];
+        const short4 L = a.lat[node];
+        const double tx = (static_cast<double>(L.x) - ct.x) * ct.z;
+        const double ty = (static_cast<double>(L.y) - ct.y) * ct.w;
+        const double tz = static_cast<double>(L.z) * rdz;
+        const int cx = cell % a.SX, cy = cell / a.SX;
+        const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            const int co = c * q.nn;
+            const double zl = a.z[dof];
+            double zv = zl, az;
+            if (q.cmask[dof]) {
+                az = zl;  // unit row: (A z)_c = z_c
+            } else {
+                az = 0.0;
+                if (s.x >= 0) az += q.Y[s.x + co] + a.Yc[s.x + co];
+                if (s.y >= 0) az += q.Y[s.y + co] + a.Yc[s.y + co];
+                if (s.z >= 0) az += q.Y[s.z + co] + a.Yc[s.z + co];
+                if (s.w >= 0) az += q.Y[s.w + co] + a.Yc[s.w + co];
+                double zcoarse = 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const double w = ((k & 1) ? tx : 1.0 - tx) * ((k & 2) ? ty : 1.0 - ty) * ((k & 4) ? tz : 1.0 - tz);
+                    zcoarse += w * __ldg(a.zc + 3 * as_corner_node(a, cx, cy, k) + c);
+                }
+                zv += zcoarse;
+            }
+            const double pn = fresh ? zv : zv + beta * q.p[dof];
+            const double apn = fresh ? az : az + beta * q.ap[dof];
+            q.p[dof] = pn;
+            q.ap[dof] = apn;
+            part += pn * apn;
+        }
+    }
+    return part;
+}
+
+// GU: the gather half (p, Ap recurrences and p.Ap; or the true residual)
+// and the update half (x, r, XL32 panel, r.r, loop head) across one
+// software grid barrier. The grid must be co-resident (host: occupancy x
+// SMs); dependents are released only after the barrier.
+__global__ void __launch_bounds__(256) as_gu_split_kernel(CgParams q, AsParams a) {
+    pdl_wait();
+    __shared__ double sh[64];
+    __shared__ bool last;
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const unsigned gen = *reinterpret_cast<volatile unsigned *>(&st->bar_gen);
+    const int yx = st->y_holds_x;
+    const bool fresh = st->fresh != 0;
+    const double rz = st->rz_l + st->rz_c;
+    const double beta = fresh ? 0.0 : rz / st->rho;
+    double part[1] = {as_gu_nodes(q, a, yx, fresh, beta)};
+    block_sum<1>(part, sh);
+    if (threadIdx.x == 0) {
+        q.partial[blockIdx.x] = part[0];
+        __threadfence();
+        last = atomicAdd(&st->ticket_a, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double tot[1];
+        grid_sum<1>(q.partial, gridDim.x, tot, sh);
+        if (threadIdx.x == 0) {
+            st->ticket_a = 0u;
+            if (!yx) {
+                st->rho = rz;  // r.z of the current residual
+                st->fresh = 0;
+                st->beta = beta;
+            }
+            cg_gather_finish(st, yx, tot[0]);
+            __threadfence();
+            atomicExch(&st->bar_gen, gen + 1u);
+        }
+    } else if (threadIdx.x == 0) {
+        while (*reinterpret_cast<volatile unsigned *>(&st->bar_gen) == gen) __nanosleep(64);
+        __threadfence();
+    }
+    __syncthreads();
+    pdl_trigger();
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int phase = *reinterpret_cast<volatile int *>(&st->phase);
+    const double alpha = *reinterpret_cast<volatile double *>(&st->alpha);
+    part[0] = as_update_nodes(q, a, phase, alpha);
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial + gridDim.x, &st->ticket_b)) return;
+    double tot[1];
+    grid_sum<1>(q.partial + gridDim.x, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_b = 0u;
+    as_update_finish(st, phase, tot[0]);
     __threadfence();
 }
 
