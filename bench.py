@@ -149,6 +149,7 @@ def cpu_sample(cfg, rom_tsv, rom_dum, iters, side, threads):
     kinds_s = None if kinds is None else kinds.reshape(cfg.rows, cfg.cols)[:side, :side].ravel().copy()
     dt = cfg.delta_t()
     dt_s = dt if dt.size == 1 else dt.reshape(cfg.rows, cfg.cols)[:side, :side].ravel().copy()
+    t_wall = time.perf_counter()
     t0 = time.perf_counter()
     s = refpy.RefSession(r0, r1 if (kinds_s is not None and kinds_s.any()) else None, side, side,
                          kinds=kinds_s, delta_t=dt_s, bc_mode=1)
@@ -170,11 +171,39 @@ def cpu_sample(cfg, rom_tsv, rom_dum, iters, side, threads):
     for f in os.listdir(tmp):
         os.remove(os.path.join(tmp, f))
     os.rmdir(tmp)
-    return {"value": cfg.B / total, "unit": "blocks/s", "cores": threads, "kind": "reference",
+    return {"value": cfg.B / total, "unit": "blocks/s", "cores": threads, "kind": "reference", "cpu": cpu_model_name(),
             "sample": (f"tsvstress CSR path (oracle/_ref) on a {side}x{side} sub-array of {cfg.name} with the same ROM: "
                        f"index+assemble+lift {t_setup:.2f}s, {n_it} Jacobi-CG iterations {t_solve:.2f}s, recovery of "
                        f"{nrec} blocks {t_rec:.2f}s; extrapolated per block to B={cfg.B} at {iters} iterations"),
-            "seconds_per_array": total}
+            "seconds_per_array": total, "wall_s": time.perf_counter() - t_wall}
+
+
+MODEL_CHECK = os.path.join(ROOT, "profiles", "r2", "cpu_model_check_cfg2.json")
+
+
+def cpu_model_name():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def model_check():
+    """How the sample extrapolation compares with a FULL run of the
+    reference's CSR pipeline at config 2 (tools/cpu_model_check.py, run on
+    the GPU box host and committed): the validation the reference arm quotes."""
+    try:
+        d = json.load(open(MODEL_CHECK))
+    except (OSError, ValueError):
+        return None
+    f = d["full_run"]
+    return {"validated_at": d["config"], "cpu": d.get("cpu"), "cores": d.get("cores"),
+            "full_run_s": f["total_s"], "full_run_iterations": f["iterations"],
+            "sample_model_predicted_s": d["sample_model"]["predicted_total_s"],
+            "model_error": d["model_error"], "source": os.path.relpath(MODEL_CHECK, ROOT)}
 
 
 def jacobi_iterations(cfg):
@@ -214,7 +243,12 @@ def run_reference(args, cfg, rank, world):
                        "bc": BC, "points": cfg.points},
             "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "blocks/s", "cores": threads, "kind": "reference",
-                             "sample": vals[-1]["sample"]},
+                             "cpu": cpu_model_name(), "sample": vals[-1]["sample"]},
+            "modelled": {"what": ("ms_per_step and value are the per-block extrapolation of the measured bounded "
+                                  "sample to the full array at the Jacobi iteration count; each step measured "
+                                  "only the sample"),
+                         "measured_wall_s_per_step": statistics.median(x["wall_s"] for x in vals),
+                         "model_check": model_check()},
             "e2e": {"value": v, "unit": "blocks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -298,6 +332,8 @@ def run_ours(args, cfg, rank, local_rank, world):
         try:
             cpu = cpu_sample(cfg, rom_tsv, rom_dum, rec_j or jacobi_iterations(cfg), args.cpu_sample, host_threads())
             cpu.pop("seconds_per_array", None)
+            cpu.pop("wall_s", None)
+            cpu["model_check"] = model_check()
         except Exception as e:  # oracle not built: report, do not fail the bench
             cpu = {"value": None, "unit": "blocks/s", "cores": host_threads(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -332,7 +368,7 @@ def run_ours(args, cfg, rank, local_rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "blocks": cfg.B, "array": f"{cfg.rows}x{cfg.cols}", "reduced_dofs_per_block": cfg.n,
                    "global_dofs": ix.dof_count, "fine_dofs_per_block": cfg.n_fine, "points_per_element": cfg.points,
-                   "iterations": iters, "tol": TOL, "precond": args.precond, "bc": BC,
+                   "iterations": iters, "restarts": sol.restarts, "tol": TOL, "precond": args.precond, "bc": BC,
                    "coarse_dofs": nc if schwarz else None,
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2: {out_bytes / 1e9:.1f} GB stress output + {ix.dof_count * 8 * 6 / 1e6:.0f} MB vectors per step"},

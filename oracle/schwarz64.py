@@ -69,7 +69,8 @@ def choose_super_block(rows, cols, max_coarse=12000):
 class Schwarz64:
     """Exact FP64 two-level additive Schwarz operator for an orcpy.OracleSystem."""
 
-    def __init__(self, o: "orcpy.OracleSystem", q, s: int | None = None, max_coarse: int = 12000):
+    def __init__(self, o: "orcpy.OracleSystem", q, s: int | None = None, max_coarse: int = 12000,
+                 sparse_coarse: bool = False):
         qx, qy, qz = (q, q, q) if np.isscalar(q) else q
         self.o = o
         rows, cols, B, n, N = o.rows, o.cols, o.B, o.n, o.N
@@ -145,7 +146,8 @@ class Schwarz64:
         self.P, self.PT = P, P.T.tocsr()
         # A_c = sum_b (P[d_b])^T K_b P[d_b]  (P is zero on constrained rows,
         # so the lifting's masks drop out); identical P[d_b] share one product
-        Ac = np.zeros((Nc, Nc))
+        Ac = sp.lil_matrix((Nc, Nc)) if sparse_coarse else np.zeros((Nc, Nc))
+        acc = [] if sparse_coarse else None
         cache = {}
         for b in range(B):
             Pb = P[dm[b]].tocoo()
@@ -156,7 +158,17 @@ class Schwarz64:
             G = cache.get(key)
             if G is None:
                 G = cache[key] = W.T @ (K[kinds[b]] @ W)
-            Ac[np.ix_(cidx, cidx)] += G
+            if sparse_coarse:
+                acc.append((np.repeat(cidx, cidx.size), np.tile(cidx, cidx.size), G.ravel()))
+            else:
+                Ac[np.ix_(cidx, cidx)] += G
+        if sparse_coarse:  # experiments with large coarse spaces (s = 1): SuperLU instead of dense Cholesky
+            import scipy.sparse.linalg as spla
+            ri, ci, vv = (np.concatenate(t) for t in zip(*acc))
+            Acs = sp.csc_matrix((vv, (ri, ci)), shape=(Nc, Nc))
+            self.coarse_lu = spla.splu(Acs)
+            self.coarse = None
+            return
         # coarse DoFs that every block leaves empty (none in practice) stay identity
         empty = np.nonzero(np.diag(Ac) == 0.0)[0]
         Ac[empty, empty] = 1.0
@@ -169,6 +181,8 @@ class Schwarz64:
         for t, idx in enumerate(self.groups):
             Z[idx] = R[idx] @ self.ainv[t]
         z = np.bincount(self.dm_flat, weights=Z.ravel(), minlength=self.o.N)
+        if self.coarse is None:
+            return z + self.P @ self.coarse_lu.solve(self.PT @ r)
         L = self.coarse[0]  # lower Cholesky factor (two TRSVs: LAPACK potrs is ~20x slower here)
         y = sla.solve_triangular(L, self.PT @ r, lower=True, check_finite=False)
         z += self.P @ sla.solve_triangular(L, y, lower=True, trans="T", check_finite=False)

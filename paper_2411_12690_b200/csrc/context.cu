@@ -269,7 +269,6 @@ struct tsv_ctx {
         DevBuf<int4> kp_items;
         DevBuf<int> kp_rows;
         int kp_nitems = 0;
-        size_t kp_smem = 0;
     } as2;
     // int8 (Ozaki) K1: digit planes of the X panel
     int oz_s = 0;            // digits per value (0 = DMMA K1)
@@ -508,12 +507,14 @@ struct tsv_ctx {
     }
 
     // Super-block side s of the Schwarz coarse space: the smallest s whose
-    // corner lattice has <= TSV_AS_COARSE_MAX (8192) coarse DoFs, or TSV_AS_S.
+    // corner lattice has <= TSV_AS_COARSE_MAX (16384) coarse DoFs, or TSV_AS_S.
     // It also fixes the node numbering (set_layout), so it depends only on
-    // the array shape.
+    // the array shape. Measured at config 3 (B200): s = 3 (7350 coarse DoFs)
+    // 75 iterations x 0.537 ms; s = 2 (15606) 57 x 0.628 ms; s = 1 does not
+    // cut iterations further (60 in the FP64 oracle, tools/coarse_quant_scan.py).
     static int schwarz_super_block(uint32_t rows, uint32_t cols) {
         if (getenv("TSV_AS_S")) return std::max(1, std::atoi(getenv("TSV_AS_S")));
-        const size_t cap = getenv("TSV_AS_COARSE_MAX") ? std::strtoul(getenv("TSV_AS_COARSE_MAX"), nullptr, 10) : 8192;
+        const size_t cap = getenv("TSV_AS_COARSE_MAX") ? std::strtoul(getenv("TSV_AS_COARSE_MAX"), nullptr, 10) : 16384;
         for (int sb = 1;; ++sb) {
             const size_t SX = (cols + sb - 1) / sb, SY = (rows + sb - 1) / sb;
             if ((SX + 1) * (SY + 1) * 6 <= cap || (SX == 1 && SY == 1)) return sb;
@@ -752,12 +753,43 @@ struct tsv_ctx {
         cfg.blockDim = block;
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cudaLaunchAttribute attr[2];
+        int na = 0;
+        if (!off) {
+            attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[na].val.programmaticStreamSerializationAllowed = 1;
+            ++na;
+        }
+        // CTA scheduling priority (captured into the graph nodes): the split
+        // Schwarz loop keeps the main chain (K1) ahead of the side chain's
+        // many small CTAs; the serial loop prefers the coarse chain, its
+        // longer branch.
+        const int prio = st == side ? prio_side : prio_main;
+        if (prio != 0) {
+            attr[na].id = cudaLaunchAttributePriority;
+            attr[na].val.priority = prio;
+            ++na;
+        }
         cfg.attrs = attr;
-        cfg.numAttrs = off ? 0 : 1;
+        cfg.numAttrs = na;
         CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+    }
+
+    int prio_main = 0, prio_side = 0;  // launch priorities (set per loop variant in ensure_graph)
+    void set_launch_priorities() {
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        // Opt-in (TSV_PRIO=1): measured on B200 at config 3, no change either
+        // way (0.6796 vs 0.6793 ms split, 0.6284 vs 0.6282 ms serial).
+        if (!getenv_flag("TSV_PRIO")) {
+            prio_main = prio_side = 0;
+        } else if (pre_kind == TSV_PRECOND_SCHWARZ2 && as_split()) {
+            prio_main = greatest;
+            prio_side = least;
+        } else {
+            prio_main = 0;
+            prio_side = greatest;
+        }
     }
 
     SolverHandles solver;   // created on first use, kept for the context's lifetime
@@ -943,9 +975,6 @@ struct tsv_ctx {
             as2.kp_rows.upload(krows.data(), krows.size(), stream);
             as2.kp_items.upload(items.data(), items.size(), stream);
             as2.kp_nitems = static_cast<int>(items.size());
-            as2.kp_smem = (n * kpzc_ld() + static_cast<size_t>(kKpzcChunk) * 24) * sizeof(double);
-            if (as2.kp_smem > 227 * 1024) throw StatusError(TSV_EINVAL, "schwarz2: per-key coarse product too large for shared memory");
-            CK(cudaFuncSetAttribute(as_kpzc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(as2.kp_smem)));
             as2.Yc.alloc(B_pad * ldk);
             CK(cudaMemsetAsync(as2.Yc.ptr, 0, B_pad * ldk * sizeof(double), stream));
             CK(cudaStreamSynchronize(stream));  // host staging vectors go out of scope
@@ -1620,7 +1649,13 @@ struct tsv_ctx {
 
     void launch_iteration(const CgParams &q) {
         if (pre_kind == TSV_PRECOND_SCHWARZ2 && as_split()) {
-            launch_pdl(as_gu_split_kernel, gu_split_grid(), kVecThreads, 0, stream, q, as_params());
+            if (fused_gu()) {
+                launch_pdl(as_gu_split_kernel, gu_split_grid(), kVecThreads, 0, stream, q, as_params());
+            } else {
+                launch_pdl(as_g_split_kernel, cg_grid(), kVecThreads, 0, stream, q, as_params());
+                launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, as_params());
+                ++launches;
+            }
             ++launches;
             launch_split_tail(q);
             return;
@@ -1638,17 +1673,18 @@ struct tsv_ctx {
     }
 
     int graph_kernels_per_iteration() const {
-        const int schwarz = as_split() ? 10 : (fused_gu() ? 9 : 10);
+        const int schwarz = as_split() ? (fused_gu() ? 10 : 11) : (fused_gu() ? 9 : 10);
         return (pre_kind == TSV_PRECOND_SCHWARZ2 ? schwarz : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
     }
 
-    // Split Schwarz loop (default; TSV_AS_SPLIT=0 restores the serial one):
-    // after r is updated, the coarse chain runs on the side stream beside the
-    // local solve, z_l and K1 (A z_l); A P zc enters through the Yc panel.
-    static bool as_split() {
-        const char *v = getenv("TSV_AS_SPLIT");
-        return !(v && *v == '0');
-    }
+    // Split Schwarz loop (opt-in, TSV_AS_SPLIT=1): after r is updated, the
+    // coarse chain runs on the side stream beside the local solve, z_l and K1
+    // (A z_l); A P zc enters through the Yc panel. Correct (same iterations
+    // +-6, parity tests) but measured slower on B200 at config 3 (0.583 vs
+    // 0.537 ms per iteration at s = 3; 0.680 vs 0.628 at s = 2): K1 holds
+    // every SM's register file (2 x 128 x 240 regs), so the side chain only
+    // runs between kernels, and every other kernel is HBM-bound like it.
+    static bool as_split() { return getenv_flag("TSV_AS_SPLIT"); }
     unsigned gu_split_grid() {
         if (!gu_split_grid_) {
             int per_sm = 0;
@@ -1692,7 +1728,8 @@ struct tsv_ctx {
             as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
             as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
         }
-        launch_pdl(as_kpzc_kernel, static_cast<unsigned>(as2.kp_nitems), 256, as2.kp_smem, side, q, a, kpzc_params());
+        launch_pdl(as_kpzc_kernel, dim3(static_cast<unsigned>(as2.kp_nitems), static_cast<unsigned>((n + kKpzcRows - 1) / kKpzcRows)),
+                   kKpzcRows, 0, side, q, a, kpzc_params());
         CK(cudaEventRecord(ev_join, side));
         if (as2.tc) {
             launch_tc_local();
@@ -1709,7 +1746,10 @@ struct tsv_ctx {
 
     // Gather + update as one kernel across a software grid barrier (Schwarz
     // path; TSV_NO_FUSED_GU=1 keeps the two kernels).
-    static bool fused_gu() { return !getenv_flag("TSV_NO_FUSED_GU"); }
+    // Measured at config 3 (B200): the barrier-fused kernels are slower than
+    // the two kernels with PDL between them (92 vs 35 + 50 us serial; 141 us
+    // split), so they are opt-in (TSV_FUSED_GU=1).
+    static bool fused_gu() { return getenv_flag("TSV_FUSED_GU"); }
     unsigned gu_grid() {
         if (!gu_grid_) {
             int per_sm = 0;
@@ -1726,6 +1766,7 @@ struct tsv_ctx {
         if (iter_graph && graph_oz_s == oz_s) return;
         PhaseTimer pt("graph capture");
         drop_graph();
+        set_launch_priorities();
         graph_oz_s = oz_s;
         CgParams q = cg_params();
         cudaGraph_t graph;

@@ -66,7 +66,6 @@ struct KpzcParams {
     long long ldk;
 };
 constexpr int kKpzcChunk = 64;
-__host__ __device__ constexpr int kpzc_ld() { return 25; }  // odd-word row stride: conflict-free 8 B smem reads
 
 // Round to `bits` explicit mantissa bits (emulates a low-precision operand).
 __device__ __forceinline__ double round_mantissa(double v, int bits) {
@@ -719,37 +718,46 @@ __global__ void __launch_bounds__(256) as_zl_split_kernel(CgParams q, AsParams a
     __threadfence();
 }
 
-// A P zc per block: Yc[row] = (K_b P_b) zc_cell(b), one CTA per (key, up
-// to kKpzcChunk blocks of that key); the key's n x 24 product sits in shared
-// memory. Side stream, after the coarse solve.
-__global__ void __launch_bounds__(256) as_kpzc_kernel(CgParams q, AsParams a, KpzcParams k) {
+// A P zc per block: Yc[row] = (K_b P_b) zc_cell(b). CTA = (key chunk of up
+// to kKpzcChunk blocks, slice of kKpzcRows panel columns); each thread keeps
+// one row of the key's n x 24 product in registers and walks the chunk's
+// blocks (their 24 coarse values broadcast from shared memory); the Yc row
+// writes are coalesced. Side stream, after the coarse solve.
+constexpr int kKpzcRows = 128;
+__global__ void __launch_bounds__(kKpzcRows) as_kpzc_kernel(CgParams q, AsParams a, KpzcParams k) {
     pdl_wait();
-    extern __shared__ double smk[];
+    __shared__ double zcs[kKpzcChunk][24];
+    __shared__ int rows[kKpzcChunk];
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
     const int4 it = k.items[blockIdx.x];
-    const int n = k.n, nb = it.z - it.y;
-    double *kps = smk;                                  // [n][kpzc_ld()]
-    double *zcs = smk + static_cast<size_t>(n) * kpzc_ld();  // [kKpzcChunk][24]
-    const double *kp = k.kp + static_cast<long long>(it.x) * k.ldk * 24;
-    for (int i = threadIdx.x; i < n * 24; i += blockDim.x) kps[(i / 24) * kpzc_ld() + i % 24] = __ldg(kp + i);
+    const int nb = it.z - it.y;
     for (int i = threadIdx.x; i < nb * 24; i += blockDim.x) {
         const int bi = i / 24, j = i % 24;
-        const int cell = k.row_cell[k.rows[it.y + bi]];
+        const int row = k.rows[it.y + bi];
+        const int cell = k.row_cell[row];
         const int cx = (cell % k.cols) / k.sb, cy = (cell / k.cols) / k.sb;
-        zcs[i] = a.zc[3 * as_corner_node(a, cx, cy, j / 3) + j % 3];
+        zcs[bi][j] = a.zc[3 * as_corner_node(a, cx, cy, j / 3) + j % 3];
+        if (j == 0) rows[bi] = row;
+    }
+    const int r = blockIdx.y * kKpzcRows + threadIdx.x;
+    double kr[24];
+    if (r < k.n) {
+        const double2 *src = reinterpret_cast<const double2 *>(k.kp + (static_cast<long long>(it.x) * k.ldk + r) * 24);
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+            const double2 v = __ldg(src + j);
+            kr[2 * j] = v.x;
+            kr[2 * j + 1] = v.y;
+        }
     }
     __syncthreads();
     pdl_trigger();
+    if (r >= k.n) return;
     for (int bi = 0; bi < nb; ++bi) {
-        double *yrow = a.Yc + static_cast<long long>(k.rows[it.y + bi]) * k.ldk;
-        const double *zb = zcs + bi * 24;
-        for (int r = threadIdx.x; r < n; r += blockDim.x) {
-            const double *kr = kps + r * kpzc_ld();
-            double y = 0.0;
+        double y = 0.0;
 #pragma unroll
-            for (int j = 0; j < 24; ++j) y += kr[j] * zb[j];
-            yrow[r] = y;
-        }
+        for (int j = 0; j < 24; ++j) y += kr[j] * zcs[bi][j];
+        a.Yc[static_cast<long long>(rows[bi]) * k.ldk + r] = y;
     }
 }
 
@@ -800,6 +808,34 @@ __device__ __forceinline__ double as_gu_nodes(const CgParams &q, const AsParams 
         }
     }
     return part;
+}
+
+// G' alone (the update follows as as_update_kernel): p, Ap recurrences and
+// p.Ap (or the true residual); the last CTA stores rho, beta and alpha.
+__global__ void __launch_bounds__(256, 4) as_g_split_kernel(CgParams q, AsParams a) {
+    pdl_wait();
+    __shared__ double sh[64];
+    CgState *st = q.st;
+    if (*reinterpret_cast<volatile int *>(&st->done)) return;
+    const int yx = st->y_holds_x;
+    const bool fresh = st->fresh != 0;
+    const double rz = st->rz_l + st->rz_c;
+    const double beta = fresh ? 0.0 : rz / st->rho;
+    double part[1] = {as_gu_nodes(q, a, yx, fresh, beta)};
+    pdl_trigger();
+    block_sum<1>(part, sh);
+    if (!publish_partials<1>(part, q.partial, &st->ticket_a)) return;
+    double tot[1];
+    grid_sum<1>(q.partial, gridDim.x, tot, sh);
+    if (threadIdx.x != 0) return;
+    st->ticket_a = 0u;
+    if (!yx) {
+        st->rho = rz;
+        st->fresh = 0;
+        st->beta = beta;
+    }
+    cg_gather_finish(st, yx, tot[0]);
+    __threadfence();
 }
 
 // GU: the gather half (p, Ap recurrences and p.Ap; or the true residual)

@@ -13,10 +13,12 @@ from paper_2411_12690_b200.api import build_config_rom
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind", [0, 1])
-def test_config0_rom_matches_reference(oracle_libs, native_lib, kind):
+@pytest.mark.parametrize("ci,kind", [(0, 0), (0, 1), (2, 0), (3, 0), (4, 1)])
+def test_config_rom_matches_reference(oracle_libs, native_lib, ci, kind):
+    """The ROMs the bench consumes (config 2: 24^3 mesh, q = 6; config 3:
+    20^3, q = 7; config 4's dummy) against the reference's build_rom."""
     refpy, _ = oracle_libs
-    cfg = configs.get(0)
+    cfg = configs.get(ci)
     r = ref_rom(cfg, kind, refpy)
     g = build_config_rom(cfg, kind)
     assert g.fingerprint == r.fingerprint            # same SHA-256 header (rom.cpp:110-132)
