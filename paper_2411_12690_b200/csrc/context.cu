@@ -384,6 +384,7 @@ struct tsv_ctx {
         // Few 128 x 64 tiles (small arrays): switch K1 to 64 x 64 tiles.
         k1_small = m_tiles * (round_up(n, kBN) / kBN) < static_cast<size_t>(k1_grid);  // fewer tiles than CTA slots
         setup_streamk();
+        prepare_k1_splitk();
 
         PhaseTimer pt_ren("  renumber+slots");
         // Node renumbering (first visit, blocks in super-cell-major order:
@@ -773,6 +774,28 @@ struct tsv_ctx {
         cfg.attrs = attr;
         cfg.numAttrs = na;
         CK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+    }
+
+    // Split-K factor of the small-array K1 (TSV_K1_SPLITK=0 disables): as many
+    // k-slices as fill the resident CTA slots once, at most one per k-chunk.
+    DevBuf<double> sk1_work;
+    DevBuf<unsigned> sk1_ticket;
+    int k1_split_k(int tiles, int k_chunks) const {
+        const char *v = getenv("TSV_K1_SPLITK");
+        if (v && *v == '0') return 1;
+        return std::min(std::min(k_chunks, kSplitKMax), std::max(1, k1s_grid / std::max(1, tiles)));
+    }
+    static constexpr int kSplitKMax = 8;
+    // buffers sized at set_layout (never inside a graph capture)
+    void prepare_k1_splitk() {
+        if (!k1_small) return;
+        const int tiles = static_cast<int>(B_pad / K1SmallCfg::BM) * static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
+        const int S = k1_split_k(tiles, static_cast<int>(ldk / K1SmallCfg::KC));
+        if (S <= 1) return;
+        const size_t need = static_cast<size_t>(tiles) * S * K1SmallCfg::FM * K1SmallCfg::FN * 2 * K1SmallCfg::THREADS;
+        if (sk1_work.count < need) sk1_work.alloc(need);
+        if (sk1_ticket.count < static_cast<size_t>(tiles)) sk1_ticket.alloc(static_cast<size_t>(tiles));
+        CK(cudaMemsetAsync(sk1_ticket.ptr, 0, sk1_ticket.count * sizeof(unsigned), stream));
     }
 
     int prio_main = 0, prio_side = 0;  // launch priorities (set per loop variant in ensure_graph)
@@ -1388,8 +1411,67 @@ struct tsv_ctx {
 
     // r update + two-level Schwarz z = M r (U', local GEMM, restriction,
     // coarse solve, prolongation + r.z).
+    // Early coarse chain (default; TSV_AS_EARLY_COARSE=0 forks after the
+    // update instead): the restriction of the new residual is formed as
+    // P^T r' = P^T r - alpha P^T (A p), so the coarse chain forks right after
+    // the gather (alpha known) and runs beside the update as well as the
+    // local solves. Restarts and the initial residual restrict r itself.
+    static bool early_coarse() {
+        const char *v = getenv("TSV_AS_EARLY_COARSE");
+        return !(v && *v == '0');
+    }
+
+    void launch_coarse_chain(const CgParams &q, const AsParams &a) {
+        if (getenv_flag("TSV_AS_RESTRICT_CTA"))
+            launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 3 * kRestrictGroup, 0, side, q, a);
+        else
+            launch_pdl(as_restrict_warp_kernel, (as2.ncells + kRestrictWarps - 1) / kRestrictWarps, 32 * kRestrictWarps, 0,
+                       side, q, a);
+        launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, side, q, a);
+        if (as2.sym_nt) {
+            const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
+            // one 64 x 64 tile per CTA (a fixed grid walking tiles with a
+            // register prefetch of the next tile measured slower: 0.655 vs
+            // 0.620 ms per iteration at config 3)
+            launch_pdl(as_coarse_symv_kernel, ntiles, 128, 0, side, q, a, static_cast<const float *>(as2.sym_tiles.ptr),
+                       as2.sym_nt, as2.sym_part.ptr);
+            launch_pdl(as_coarse_symv_reduce_kernel, as2.sym_nt, kSymRedG * kSymT, 0, side, q, a, as2.sym_nt,
+                       static_cast<const double *>(as2.sym_part.ptr));
+        } else {
+            as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
+            as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
+        }
+    }
+
+    void launch_local_solve() {
+        if (as2.tc) {
+            launch_tc_local();
+        } else {
+            GemmParams gp = local_gemm_params();
+            gemm_nt_f64<K1SmallCfg><<<std::min(k1s_grid, gp.m_tiles * gp.n_tiles), K1SmallCfg::THREADS, K1SmallCfg::SMEM,
+                                      stream>>>(gp);
+        }
+    }
+
     void launch_as_update_precond(const CgParams &q, bool with_gather) {
         AsParams a = as_params();
+        if (with_gather && !fused_gu() && early_coarse()) {
+            // gather -> fork {coarse chain on P^T r - alpha P^T Ap} || {update
+            // -> local solves -> z_l} -> join
+            launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
+            CK(cudaEventRecord(ev_fork, stream));
+            CK(cudaStreamWaitEvent(side, ev_fork, 0));
+            AsParams ae = a;
+            ae.rc_recur = 1;
+            launch_coarse_chain(q, ae);
+            CK(cudaEventRecord(ev_join, side));
+            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+            launch_local_solve();
+            launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+            CK(cudaStreamWaitEvent(stream, ev_join, 0));
+            launches += 7;
+            return;
+        }
         // r update (grid-stride). Fusing the coarse restriction in (warp-level
         // per-cell partials) measured slower at config 3: 80 us vs 47 + 34 us
         // with the restriction off the critical path on the side stream.
@@ -1407,26 +1489,9 @@ struct tsv_ctx {
         // forked graph.
         CK(cudaEventRecord(ev_fork, stream));
         CK(cudaStreamWaitEvent(side, ev_fork, 0));
-        launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 3 * kRestrictGroup, 0, side, q, a);
-        launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, side, q, a);
-        if (as2.sym_nt) {
-            const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
-            launch_pdl(as_coarse_symv_kernel, ntiles, 128, 0, side, q, a, static_cast<const float *>(as2.sym_tiles.ptr),
-                       as2.sym_nt, as2.sym_part.ptr);
-            launch_pdl(as_coarse_symv_reduce_kernel, as2.sym_nt, kSymRedG * kSymT, 0, side, q, a, as2.sym_nt,
-                       static_cast<const double *>(as2.sym_part.ptr));
-        } else {
-            as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
-            as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
-        }
+        launch_coarse_chain(q, a);
         CK(cudaEventRecord(ev_join, side));
-        if (as2.tc) {
-            launch_tc_local();
-        } else {
-            GemmParams gp = local_gemm_params();
-            gemm_nt_f64<K1SmallCfg><<<std::min(k1s_grid, gp.m_tiles * gp.n_tiles), K1SmallCfg::THREADS, K1SmallCfg::SMEM,
-                                      stream>>>(gp);
-        }
+        launch_local_solve();
         // the local part of z (and r.z_l) while the coarse chain finishes
         launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
         CK(cudaStreamWaitEvent(stream, ev_join, 0));
@@ -1608,9 +1673,17 @@ struct tsv_ctx {
             gp.n_tiles = static_cast<int>(round_up(n, K1SmallCfg::BN) / K1SmallCfg::BN);
             gp.k_chunks = static_cast<int>(ldk / K1SmallCfg::KC);
             gp.tile_kind = tile_kind_small_d.ptr;
-            // no more CTAs than tiles: idle CTAs would only contend on the tile counter
-            const int g = std::min(k1s_grid, gp.m_tiles * gp.n_tiles);
-            launch_pdl(gemm_nt_f64<K1SmallCfg>, g, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream, gp);
+            const int tiles = gp.m_tiles * gp.n_tiles;
+            const int S = k1_split_k(tiles, gp.k_chunks);
+            if (S > 1) {
+                // split-K: tiles x S CTAs fill the resident slots (one wave)
+                SplitK sk{sk1_work.ptr, sk1_ticket.ptr, S};
+                launch_pdl(gemm_splitk_f64<K1SmallCfg>, tiles * S, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream, gp, sk);
+            } else {
+                // no more CTAs than tiles: idle CTAs would only contend on the tile counter
+                const int g = std::min(k1s_grid, tiles);
+                launch_pdl(gemm_nt_f64<K1SmallCfg>, g, K1SmallCfg::THREADS, K1SmallCfg::SMEM, stream, gp);
+            }
         } else if (k1_streamk) {
             StreamK sk{sk_start.ptr, sk_work.ptr, sk_flag.ptr};
             launch_pdl(gemm_streamk_f64<K1Cfg>, k1_grid, K1Cfg::THREADS, K1Cfg::SMEM, stream, gp, sk);
@@ -2209,6 +2282,8 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         CK(cudaFuncSetAttribute(gemm_streamk_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1Cfg::SMEM)));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1SmallCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(K1SmallCfg::SMEM)));
+        CK(cudaFuncSetAttribute(gemm_splitk_f64<K1SmallCfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1SmallCfg::SMEM)));
         int occ_s = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, gemm_nt_f64<K1SmallCfg>, K1SmallCfg::THREADS,

@@ -263,6 +263,75 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
     }
 }
 
+// Split-K DMMA GEMM for arrays with fewer tiles than SM slots (configs
+// 0-2: 5-128 tiles of 64 x 64): CTA (tile, s) accumulates the k-chunks
+// [s kc / S, (s+1) kc / S), parks its accumulators in work (thread-major,
+// coalesced) and takes a per-tile ticket; the last of the S CTAs sums the
+// S partials in s order (fixed: bitwise reproducible) and runs the epilogue.
+struct SplitK {
+    double *work;      // [tiles * S][FM*FN*2][THREADS]
+    unsigned *ticket;  // [tiles], zero between launches
+    int S;
+};
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_splitk_f64(GemmParams p, SplitK sk) {
+    pdl_wait();
+    extern __shared__ __align__(16) double smem[];
+    __shared__ bool last;
+    double *As = smem;
+    double *Bs = smem + Cfg::STAGES * Cfg::A_STAGE;
+    constexpr int NACC = Cfg::FM * Cfg::FN * 2;
+    const int tid = threadIdx.x;
+    if ((p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) ||
+        (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0))
+        return;
+    const int S = sk.S;
+    const int tile = blockIdx.x / S, s = blockIdx.x % S;
+    const int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+    const int kc0 = (p.k_chunks * s) / S, kc1 = (p.k_chunks * (s + 1)) / S;
+    double acc[Cfg::FM][Cfg::FN][2];
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    gemm_segment<Cfg>(p, As, Bs, mt, nt, kc0, kc1, gemm_fn_lim<Cfg>(p, nt), acc);
+    double *w = sk.work + static_cast<long long>(blockIdx.x) * NACC * Cfg::THREADS;
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) w[((i * Cfg::FN + j) * 2 + h) * Cfg::THREADS + tid] = acc[i][j][h];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(&sk.ticket[tile], 1u) == static_cast<unsigned>(S - 1);
+    __syncthreads();
+    pdl_trigger();
+    if (!last) return;
+    __threadfence();
+    const double *w0 = sk.work + static_cast<long long>(tile) * S * NACC * Cfg::THREADS + tid;
+#pragma unroll
+    for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // s outer, all NACC loads of one partial in flight together
+    for (int s2 = 0; s2 < S; ++s2) {
+        const double *ws = w0 + static_cast<long long>(s2) * NACC * Cfg::THREADS;
+        double v[NACC];
+#pragma unroll
+        for (int e = 0; e < NACC; ++e) v[e] = __ldcg(ws + e * Cfg::THREADS);
+#pragma unroll
+        for (int i = 0; i < Cfg::FM; ++i)
+#pragma unroll
+            for (int j = 0; j < Cfg::FN; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) acc[i][j][h] += v[(i * Cfg::FN + j) * 2 + h];
+    }
+    gemm_epilogue<Cfg>(p, mt, nt, acc);
+    if (tid == 0) sk.ticket[tile] = 0u;
+}
+
 // Stream-K DMMA GEMM: CTA g owns the linear (tile, k-chunk) iterations
 // [start[g], start[g+1]) (host-balanced by DMMA work), so every SM finishes
 // together instead of idling through a partial last wave. A tile split

@@ -52,6 +52,9 @@ struct AsParams {
     // split loop: A P zc as a block panel (same layout as Y), from the
     // per-key products K_b P_b (as_kpzc_kernel)
     double *Yc;
+    // early coarse chain: in a NORMAL phase the restriction reads A p and the
+    // coarse rhs becomes rc - alpha P^T (A p) (forked before the r update)
+    int rc_recur;
 };
 
 // as_kpzc_kernel work: per-key K_b P_b ([key][ldk][24], internal row order
@@ -304,9 +307,11 @@ __global__ void __launch_bounds__(3 * kRestrictGroup) as_restrict_kernel(CgParam
     double acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+    // early coarse chain: A p in a NORMAL phase (rc recurrence), else r
+    const double *src = (a.rc_recur && q.st->phase == PH_NORMAL) ? q.ap : q.r;
     for (int node = nb + lt; node < ne; node += kRestrictGroup) {
         const long long dof = static_cast<long long>(c) * N + node;
-        const double r0 = __ldg(q.r + dof);  // loaded unconditionally: no cmask -> r dependency
+        const double r0 = __ldg(src + dof);  // loaded unconditionally: no cmask -> r dependency
         const double rv = __ldg(q.cmask + dof) ? 0.0 : r0;
         double w[8];
         as_cell_weights(a, cc, node, w);
@@ -330,6 +335,54 @@ __global__ void __launch_bounds__(3 * kRestrictGroup) as_restrict_kernel(CgParam
     }
 }
 
+// Restriction with one warp per coarse cell (8 cells per CTA): a lane
+// walks its cell's contiguous node range with stride 32 and keeps all 24
+// weighted sums (3 components x 8 corners); one warp reduction per sum.
+// A single wave of short-lived warps instead of thousands of CTAs whose
+// block reductions dominate (as_restrict_kernel); TSV_AS_RESTRICT_CTA=1
+// keeps the CTA-per-cell kernel.
+constexpr int kRestrictWarps = 8;
+__global__ void __launch_bounds__(32 * kRestrictWarps) as_restrict_warp_kernel(CgParams q, AsParams a) {
+    pdl_wait();
+    if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
+    const int N = q.n_nodes;
+    const int lane = threadIdx.x & 31;
+    const int cell = blockIdx.x * kRestrictWarps + (threadIdx.x >> 5);
+    if (cell >= a.ncells) return;
+    const AsCell cc = as_cell(a, cell);
+    const int nb = a.cell_ptr[cell], ne = a.cell_ptr[cell + 1];
+    const double *src = (a.rc_recur && q.st->phase == PH_NORMAL) ? q.ap : q.r;
+    double acc[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[c][k] = 0.0;
+#pragma unroll 2
+    for (int node = nb + lane; node < ne; node += 32) {
+        double rv[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            const double r0 = __ldg(src + dof);
+            rv[c] = __ldg(q.cmask + dof) ? 0.0 : r0;
+        }
+        double w[8];
+        as_cell_weights(a, cc, node, w);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[c][k] += w[k] * rv[c];
+    }
+    pdl_trigger();
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double v = warp_sum(acc[c][k]);
+            if (lane == 3 * k + c) a.cellpart[cell * 24 + 3 * k + c] = v;
+        }
+}
+
 // Coarse right-hand side: each coarse DoF sums its (up to 4) cells in order.
 __global__ void as_coarse_rhs_kernel(CgParams q, AsParams a) {
     pdl_wait();
@@ -349,7 +402,10 @@ __global__ void as_coarse_rhs_kernel(CgParams q, AsParams a) {
                 s += a.cellpart[((cy * a.SX + cx) * kAsSplit + part) * 24 + 3 * corner + comp];
         }
     }
-    a.rc[j] = s;
+    if (a.rc_recur && q.st->phase == PH_NORMAL)
+        a.rc[j] -= q.st->alpha * s;  // P^T r' = P^T r - alpha P^T (A p)
+    else
+        a.rc[j] = s;
 }
 
 // Coarse solve zc = A_c^-1 rc (fixed-order reductions): a CTA of 8 warps
