@@ -46,6 +46,7 @@ def algorithmic_bytes(cfg, N_dofs, nc, ntypes, local_rows):
         "as_update_kernel": 4 * vec + 2 * vec + slots + cmask + panel32,
         # r, cmask, lat -> 24 partials per coarse cell
         "as_restrict_kernel": vec + cmask + lat,
+        "as_restrict_warp_kernel": vec + cmask + lat,
         "as_coarse_rhs_kernel": 8 * nc * 4 + 8 * nc,
         # packed FP32 lower triangle of A_c^-1 + partials written
         "as_coarse_symv_kernel": tiles + part,
@@ -90,9 +91,11 @@ def main():
                 "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3}.get(u, 1)
     w = csv.writer(sys.stdout)
     w.writerow(["kernel", "time_us", "dram_read_MB", "dram_write_MB", "dram_GBps", "dram_frac",
-                "algorithmic_MB", "algorithmic_GBps", "algorithmic_frac", "grid", "regs", "warps_active_pct"])
+                "algorithmic_MB", "algorithmic_GBps", "algorithmic_frac", "grid", "regs", "warps_active_pct",
+                "dmma_TFLOPs"])
+    k1_flop = 2.0 * cfg.n ** 2 * cfg.B
     for r in rows[2:]:
-        name = col(r, "Kernel Name").split("(")[0].split("<")[0].strip()
+        name = col(r, "Kernel Name").split("(")[0].split("<")[0].replace("void ", "").split("::")[-1].strip()
         t = float(col(r, "gpu__time_duration.sum")) * scale("gpu__time_duration.sum")
         rd = float(col(r, "dram__bytes_read.sum")) * scale("dram__bytes_read.sum")
         wr = float(col(r, "dram__bytes_write.sum")) * scale("dram__bytes_write.sum")
@@ -101,7 +104,8 @@ def main():
                     f"{(rd + wr) / t / 1e9 / hbm:.3f}", f"{alg / 1e6:.1f}" if alg else "",
                     f"{alg / t / 1e9:.0f}" if alg else "", f"{alg / t / 1e9 / hbm:.3f}" if alg else "",
                     col(r, "launch__grid_size"), col(r, "launch__registers_per_thread"),
-                    col(r, "sm__warps_active.avg.pct_of_peak_sustained_active")])
+                    col(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                    f"{k1_flop / t / 1e12:.1f}" if name == "gemm_nt_f64" else ""])
 
 
 if __name__ == "__main__":
