@@ -32,6 +32,7 @@
 #include "kernels.cuh"
 #include "schwarz.cuh"
 #include "ozaki.cuh"
+#include "small_pcg.cuh"
 
 #include <cublas_v2.h>
 #include <cusolverDn.h>
@@ -1178,7 +1179,7 @@ struct tsv_ctx {
             for (auto &th : pool) th.join();
         }
         tick("local assembly (host)");
-        as2.tc = !getenv_flag("TSV_AS_LOCAL_F64") && as_round_bits() == 0;
+        as2.tc = !getenv_flag("TSV_AS_LOCAL_F64") && as_round_bits() == 0 && !small_pcg_candidate();
         const size_t rowsK = round_up(n, kBN);
         if (as2.tc) {
             as2.KP = static_cast<int>(round_up(n, kTcBK));
@@ -1547,11 +1548,10 @@ struct tsv_ctx {
     }
 
     // ------------------------------------------------ int8 (Ozaki) K1
-    // K1 variants. Default: FP64 DMMA for every product, except that with the
-    // Schwarz preconditioner the A x of the true-residual check runs on the
-    // int8 tensor cores with 10 Ozaki digits (exact int32 accumulation: a more
-    // accurate residual, so fewer spurious restarts at tol 1e-12; config 3:
-    // 72 iterations / 1 restart instead of 84 / 5).
+    // K1 variants. Default: FP64 DMMA for every product. Opt-in: the A x of the
+    // true-residual check on the int8 tensor cores with 10 Ozaki digits (exact
+    // int32 accumulation: a more accurate residual; in round 1, with the s = 3
+    // coarse space, 72 iterations / 1 restart instead of 84 / 5 at config 3).
     //   TSV_K1_VERIFY=0|9|10  hybrid off / digits (any preconditioner)
     //   TSV_K1_OZAKI=9|10     every K1 on the int8 tensor cores
     int oz_verify_digits() const {
@@ -1559,7 +1559,12 @@ struct tsv_ctx {
             const int s = std::atoi(v);
             return (s == 9 || s == 10) ? s : 0;
         }
-        return pre_kind == TSV_PRECOND_SCHWARZ2 ? 10 : 0;
+        // Default off since round 2: with the s = 2 coarse space the FP64 DMMA
+        // check restarts no more often than the exact int8 one (config 3: 57
+        // iterations / 1 restart either way; configs 0-4 unchanged), and the two
+        // early-exit int8 launches per iteration cost 3-8% (B200: config 3
+        // 195.7 k vs 190.0 k blocks/s, config 1 38.3 k vs 35.6 k).
+        return 0;
     }
 
     int oz_digits_env() const {
@@ -1926,7 +1931,79 @@ struct tsv_ctx {
         return status;
     }
 
+    // ------------------------------------------- persistent small-array PCG
+    // Opt-in (TSV_SMALL_PCG=1, small-tile arrays): the whole Schwarz PCG as
+    // one cooperative kernel (small_pcg.cuh) with FP64 local solves. Correct
+    // (parity suites pass, same iteration counts) but measured slower than the
+    // graph path on B200: config 0 54.5 vs 47.6 us per iteration, config 1
+    // 59.3 vs 55.6 (148 CTAs; 296 / 74 / 32 / 16 CTAs slower still): the
+    // split-K GEMM items inside the kernel are latency-bound and each of the
+    // ~10 grid barriers per iteration costs more than a PDL kernel boundary.
+    bool small_pcg_candidate() const {
+        const char *v = getenv("TSV_SMALL_PCG");
+        return v && *v == '1' && k1_small && coop_launch;
+    }
+    bool small_pcg_active() const { return pre_kind == TSV_PRECOND_SCHWARZ2 && !as2.tc && small_pcg_candidate(); }
+    int coop_launch = 0;
+    unsigned small_grid = 0;
+    DevBuf<double> small_w1, small_wl, small_gpart;
+
+    CgState run_small_pcg(double tol, int max_it) {
+        CgState s{};
+        s.done = CG_RUNNING;
+        s.phase = PH_INIT;
+        s.tol = tol;
+        s.max_it = max_it;
+        *h_state = s;
+        CK(cudaMemcpyAsync(state.ptr, h_state, sizeof(CgState), cudaMemcpyHostToDevice, stream));
+        CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), stream));
+        using Cfg = K1SmallCfg;
+        auto kern = pcg_small_kernel<Cfg>;
+        if (!small_grid) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::SMEM)));
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS, Cfg::SMEM));
+            if (per_sm < 1) throw StatusError(TSV_ECUDA, "pcg_small_kernel: no resident CTA");
+            const char *cv = getenv("TSV_SMALL_PCG_CTAS");  // grid barriers: fewer CTAs, cheaper
+            const int cap = cv ? std::max(1, std::atoi(cv)) : sm_count;
+            small_grid = static_cast<unsigned>(std::min(per_sm * sm_count, cap));
+        }
+        SmallPcgParams P{};
+        P.q = cg_params();
+        P.a = as_params();
+        P.k1 = k1_params(nullptr);
+        P.k1.m_tiles = static_cast<int>(B_pad / Cfg::BM);
+        P.k1.n_tiles = static_cast<int>(round_up(n, Cfg::BN) / Cfg::BN);
+        P.k1.k_chunks = static_cast<int>(ldk / Cfg::KC);
+        P.k1.tile_kind = tile_kind_small_d.ptr;
+        P.loc = local_gemm_params();
+        P.k1_tiles = P.k1.m_tiles * P.k1.n_tiles;
+        P.loc_tiles = P.loc.m_tiles * P.loc.n_tiles;
+        auto slices = [&](int tiles, int kc) {
+            return std::max(1, std::min(std::min(kc, kSplitKMax), static_cast<int>(small_grid) / std::max(1, tiles)));
+        };
+        P.sk1.S = slices(P.k1_tiles, P.k1.k_chunks);
+        P.skl.S = slices(P.loc_tiles, P.loc.k_chunks);
+        constexpr size_t per = static_cast<size_t>(Cfg::FM) * Cfg::FN * 2 * Cfg::THREADS;
+        const size_t n1 = static_cast<size_t>(P.k1_tiles) * P.sk1.S * per, nl = static_cast<size_t>(P.loc_tiles) * P.skl.S * per;
+        if (small_w1.count < n1) small_w1.alloc(n1);
+        if (small_wl.count < nl) small_wl.alloc(nl);
+        if (small_gpart.count < 4 * static_cast<size_t>(small_grid)) small_gpart.alloc(4 * static_cast<size_t>(small_grid));
+        P.sk1.work = small_w1.ptr;
+        P.skl.work = small_wl.ptr;
+        P.ainv_c = as2.ainv_c.ptr;
+        P.gpart = small_gpart.ptr;
+        void *args[] = {&P};
+        CK(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(small_grid), dim3(Cfg::THREADS), args, Cfg::SMEM,
+                                       stream));
+        ++launches;
+        CK(cudaMemcpyAsync(h_state, state.ptr, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        return *h_state;
+    }
+
     CgState run_cg(double tol, int max_it) {
+        if (small_pcg_active()) return run_small_pcg(tol, max_it);
         ensure_graph();
         CgState s{};
         s.done = CG_RUNNING;
@@ -2278,6 +2355,7 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         CK(cudaEventCreate(&ctx->ev1));
         CK(cudaMallocHost(&ctx->h_state, sizeof(CgState)));
         CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaDeviceGetAttribute(&ctx->coop_launch, cudaDevAttrCooperativeLaunch, device));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(K1Cfg::SMEM)));
         CK(cudaFuncSetAttribute(gemm_nt_f64<K6Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,

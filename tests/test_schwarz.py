@@ -49,6 +49,7 @@ def test_tensor_core_local_solve_matches_fp64(oracle_libs, native_lib, monkeypat
     rng = np.random.default_rng(11)
     kinds = (rng.random(20) < 0.3).astype(np.uint8) if case == "mixed" else None
     out = {}
+    monkeypatch.setenv("TSV_SMALL_PCG", "0")  # the graph path (the persistent small-array path is FP64 only)
     for mode in ("f64", "tf32"):
         if mode == "f64":
             monkeypatch.setenv("TSV_AS_LOCAL_F64", "1")
