@@ -249,6 +249,23 @@ int tsv_fp64_peak(int device, double *dmma_tflops, double *dfma_tflops);
 int tsv_profile_apply(tsv_ctx *ctx, int reps, double *ms_per_launch);
 int tsv_get_timing(tsv_ctx *ctx, tsv_timing *out);
 
+/* Mirror symmetry of the loaded ROMs (csrc/symmetry.hpp). A macro-element
+ * whose grid and materials are symmetric about its three mid-planes has
+ * K_r and Phi block diagonal over the 8 irreps of Z2^3; tsv_set_rom checks
+ * that numerically and the layout then runs K1 / K6 as 8 irrep GEMMs with
+ * 1/8 of the FP64 FLOPs (the rounding-level defect K_r - K_sym is added back
+ * on the tensor cores, so the operator stays the reference's K_r).
+ * TSV_SYM=0 disables the path. */
+typedef struct tsv_symmetry_info {
+    int recovery_symmetric;   /* K6 on the irrep path for this layout */
+    int operator_symmetric;   /* K1 on the irrep path for this layout */
+    int defect_correction;    /* K_r - K_sym carried as a TF32 term */
+    int irrep_dofs[8];        /* reduced DoFs per irrep */
+    double defect_k[2];       /* per kind: max off-block |K''| / max |K''| */
+    double defect_phi[2];
+} tsv_symmetry_info;
+int tsv_get_symmetry(tsv_ctx *ctx, tsv_symmetry_info *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -333,6 +333,14 @@ class GpuGlobalStage:
         self._check(self._L.tsv_profile_apply(self._h, reps, C.byref(ms)), "profile_apply")
         return ms.value
 
+    def symmetry(self) -> dict:
+        """Which contractions run on the mirror-symmetric (8 irrep) path."""
+        t = native.SymmetryInfo()
+        self._check(self._L.tsv_get_symmetry(self._h, C.byref(t)))
+        return dict(recovery=bool(t.recovery_symmetric), operator=bool(t.operator_symmetric),
+                    correction=bool(t.defect_correction), irrep_dofs=list(t.irrep_dofs),
+                    defect_k=list(t.defect_k), defect_phi=list(t.defect_phi))
+
     def timing(self) -> Timing:
         t = Timing()
         self._check(self._L.tsv_get_timing(self._h, C.byref(t)))

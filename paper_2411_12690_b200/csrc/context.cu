@@ -33,6 +33,8 @@
 #include "schwarz.cuh"
 #include "ozaki.cuh"
 #include "small_pcg.cuh"
+#include "sym.cuh"
+#include "symmetry.hpp"
 
 #include <cublas_v2.h>
 #include <cusolverDn.h>
@@ -188,7 +190,58 @@ struct RomHost {
     int oz_s = 0;
     DevBuf<int8_t> oz_b;
     DevBuf<int> oz_eb;
+    // Mirror symmetry (symmetry.hpp, sym.cuh): set when K_r and the dense basis
+    // rows are block diagonal over the 8 irreps to rounding.
+    bool sym = false;
+    SymTables sred, sfine;           // reduced DoFs (panel order) / dense fine DoFs
+    double sym_defect_k = 0.0, sym_defect_phi = 0.0;
+    std::vector<GemmSeg> k1_segs, k6_segs;
+    int k1_tiles_per_m = 0, k6_tiles_per_m = 0;
+    DevBuf<double> d_ks, d_phis, d_uts;   // packed K''_r / Phi''_r blocks, H u_T (fine segmented layout)
+    DevBuf<short> d_ssrc, d_sdst;         // reduced orbit tables
+    DevBuf<int> d_fsrc, d_fdst;           // fine orbit tables (U column / Us column)
+    DevBuf<GemmSeg> d_k1_segs, d_k6_segs;
+    // K_r - K_sym (the rounding-level symmetry defect of K_r), TF32, times 2^d_exp:
+    // added back on the tensor cores so the operator stays the reference's K_r
+    std::vector<float> d32_host;          // [n][n] panel order, scaled
+    int d_exp = 0;
+    bool d_nonzero = false;
 };
+
+// Symmetry-adapted packing of one ROM (tsv_set_rom): host tables from
+// SymRomPack (symmetry.hpp), uploaded here.
+void build_rom_symmetry(RomHost &m, const std::vector<double> &kp, const double *basis, const double *thermal,
+                        const std::vector<int> &dmap, cudaStream_t stream, int bn, int kc) {
+    m.sym = false;
+    const char *env = std::getenv("TSV_SYM");
+    if (env && *env == '0') return;
+    SymRomPack pk;
+    const int cells[3] = {static_cast<int>(m.cells[0]), static_cast<int>(m.cells[1]), static_cast<int>(m.cells[2])};
+    const bool ok = pk.build(m.q, cells, m.n, kp, basis, thermal, dmap, bn, kc);
+    m.sym_defect_k = pk.defect_k;
+    m.sym_defect_phi = pk.defect_phi;
+    if (!ok) return;
+    m.sred = std::move(pk.red);
+    m.sfine = std::move(pk.fine);
+    m.k1_segs = std::move(pk.k1_segs);
+    m.k6_segs = std::move(pk.k6_segs);
+    m.k1_tiles_per_m = pk.k1_tiles_per_m;
+    m.k6_tiles_per_m = pk.k6_tiles_per_m;
+    m.d32_host = std::move(pk.d32);
+    m.d_exp = pk.d_exp;
+    m.d_nonzero = pk.d_nonzero;
+    m.d_ks.upload(pk.ks.data(), pk.ks.size(), stream);
+    m.d_phis.upload(pk.ps.data(), pk.ps.size(), stream);
+    m.d_uts.upload(pk.uts.data(), pk.uts.size(), stream);
+    m.d_ssrc.upload(pk.ssrc.data(), pk.ssrc.size(), stream);
+    m.d_sdst.upload(pk.sdst.data(), pk.sdst.size(), stream);
+    m.d_fsrc.upload(pk.fsrc.data(), pk.fsrc.size(), stream);
+    m.d_fdst.upload(m.sfine.dst.data(), m.sfine.dst.size(), stream);
+    m.d_k1_segs.upload(m.k1_segs.data(), m.k1_segs.size(), stream);
+    m.d_k6_segs.upload(m.k6_segs.data(), m.k6_segs.size(), stream);
+    CK(cudaStreamSynchronize(stream));
+    m.sym = true;
+}
 
 }  // namespace
 
@@ -231,6 +284,7 @@ struct tsv_ctx {
     DevBuf<uint8_t> cmask, row_kind_d, tile_kind_d, tile_kind_small_d;
     DevBuf<unsigned> tile_counter;
     DevBuf<CgState> state;
+    DevBuf<int> zero_flag;  // a device int that stays 0 (kernels with a mandatory done flag, outside a solve)
     int pre_kind = -1;
     bool solution_valid = false;
     int stress_points = 0;
@@ -271,6 +325,23 @@ struct tsv_ctx {
         DevBuf<int> kp_rows;
         int kp_nitems = 0;
     } as2;
+    // mirror-symmetric ROMs (sym.cuh): irrep-segmented operand / product panels
+    struct SymCtx {
+        bool on = false;   // every ROM of the layout is mirror-symmetric (K6 path)
+        bool k1 = false;   // K1 on the symmetric path too
+        int tab_kind = 0;  // ROM whose (shared) reduced tables are used
+        int lds = 0;       // row length of the segmented reduced panel
+        size_t panel_smem = 0;
+        DevBuf<double> Xs, Ys, Us;
+        // K_r symmetry-defect correction on tcgen05 (TF32): Yc32 = X32 D32^T
+        bool corr = false;
+        int KP = 0, NP = 0, BN = 0, ntn = 0, LD = 0, npairs = 0;
+        double c_scale = 0.0;
+        DevBuf<float> X32, Yc32, d32;
+        DevBuf<int> tile_type;
+        DevBuf<int2> pairs;
+        CUtensorMap tmA{}, tmB{};
+    } sym;
     // int8 (Ozaki) K1: digit planes of the X panel
     int oz_s = 0;            // digits per value (0 = DMMA K1)
     int graph_oz_s = 0;      // K1 variant baked into the captured graph
@@ -460,11 +531,130 @@ struct tsv_ctx {
         }
         const size_t vec_blocks = (nodes + kVecThreads - 1) / kVecThreads;
         partial.alloc(2 * std::max<size_t>(vec_blocks, 1));
+        setup_symmetry(need);
         layout_set = true;
         bc_set = false;
         set_bc_mask(std::vector<uint8_t>(N, 0), {});
         bc_set = false;
         CK(cudaStreamSynchronize(s));
+    }
+
+    // Mirror-symmetric path (sym.cuh): on when every ROM the layout uses passed
+    // the symmetry check in tsv_set_rom and the kinds share the reduced tables.
+    void setup_symmetry(const bool need[2]) {
+        sym.on = sym.k1 = sym.corr = false;
+        const RomHost *first = nullptr;
+        for (int k = 0; k < 2; ++k) {
+            if (!need[k]) continue;
+            if (!rom[k].sym) return;
+            if (first && (first->sred.src != rom[k].sred.src || first->sred.dst != rom[k].sred.dst)) return;
+            if (!first) first = &rom[k];
+        }
+        if (!first || static_cast<size_t>(first->sred.n) != n) return;
+        sym.on = true;
+        sym.tab_kind = static_cast<int>(first - rom);
+        sym.lds = first->sred.ld;
+        sym.panel_smem = sym_panel_smem(first->sred.n_orbits, static_cast<int>(ldk), sym.lds);
+        if (sym.panel_smem > 227 * 1024) {
+            sym.on = false;
+            return;
+        }
+        CK(cudaFuncSetAttribute(sym_panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sym.panel_smem)));
+        CK(cudaFuncSetAttribute(sym_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sym.panel_smem)));
+        CK(cudaFuncSetAttribute(gemm_seg_f64<K1Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(K1Cfg::SMEM)));
+        CK(cudaFuncSetAttribute(gemm_seg_f64<K6Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(K6Cfg::SMEM)));
+        sym.Xs.alloc(B_pad * static_cast<size_t>(sym.lds));
+        CK(cudaMemsetAsync(sym.Xs.ptr, 0, sym.Xs.count * sizeof(double), stream));
+        const char *env = std::getenv("TSV_SYM_K1");
+        sym.k1 = env ? *env == '1' : !k1_small;  // TSV_SYM_K1=1 forces it on small arrays too (tests)
+        if (!sym.k1) return;
+        sym.Ys.alloc(B_pad * static_cast<size_t>(sym.lds));
+        CK(cudaMemsetAsync(sym.Ys.ptr, 0, sym.Ys.count * sizeof(double), stream));
+        // correction operand: D32[kind][NP][KP] (the tc_local layout), one common scale
+        bool any = false;
+        int e = 0;
+        for (int k = 0; k < 2; ++k)
+            if (need[k] && rom[k].d_nonzero) {
+                e = any ? std::min(e, rom[k].d_exp) : rom[k].d_exp;
+                any = true;
+            }
+        const char *envc = std::getenv("TSV_SYM_CORR");
+        if (!any || (envc && *envc == '0')) return;
+        sym.corr = true;
+        sym.c_scale = std::ldexp(1.0, -e);
+        sym.KP = static_cast<int>(round_up(n, kTcBK));
+        sym.ntn = static_cast<int>((n + 255) / 256);
+        sym.BN = static_cast<int>(round_up((n + sym.ntn - 1) / sym.ntn, 16));
+        sym.NP = sym.ntn * sym.BN;
+        sym.LD = std::max(sym.KP, sym.NP);
+        std::vector<float> d32(static_cast<size_t>(2) * sym.NP * sym.KP, 0.f);
+        for (int k = 0; k < 2; ++k) {
+            const RomHost &m = need[k] ? rom[k] : *first;
+            if (!m.d_nonzero) continue;
+            const float sc = std::ldexp(1.0f, e - m.d_exp);
+            for (size_t a = 0; a < n; ++a)
+                for (size_t b = 0; b < n; ++b) {
+                    uint32_t u;
+                    const float v = m.d32_host[a * n + b] * sc;
+                    std::memcpy(&u, &v, 4);
+                    u = (u + 0x1000u) & 0xffffe000u;  // round to TF32 (10 mantissa bits)
+                    float w;
+                    std::memcpy(&w, &u, 4);
+                    d32[(static_cast<size_t>(k) * sym.NP + a) * sym.KP + b] = w;
+                }
+        }
+        sym.d32.upload(d32.data(), d32.size(), stream);
+        if (B_pad * static_cast<size_t>(sym.LD) >= 0x7fffffffULL) {
+            sym.corr = sym.k1 = false;
+            return;
+        }
+        sym.X32.alloc(B_pad * static_cast<size_t>(sym.LD));
+        sym.Yc32.alloc(B_pad * static_cast<size_t>(sym.LD));
+        CK(cudaMemsetAsync(sym.X32.ptr, 0, sym.X32.count * sizeof(float), stream));
+        CK(cudaMemsetAsync(sym.Yc32.ptr, 0, sym.Yc32.count * sizeof(float), stream));
+        std::vector<int> tt(tile_kind.begin(), tile_kind.end());
+        sym.tile_type.upload(tt.data(), tt.size(), stream);
+        std::vector<int2> pr;
+        for (size_t i = 0; i < tt.size();) {
+            if (i + 1 < tt.size() && tt[i + 1] == tt[i]) {
+                pr.push_back(make_int2(static_cast<int>(i), static_cast<int>(i + 1)));
+                i += 2;
+            } else {
+                pr.push_back(make_int2(static_cast<int>(i), -1));
+                i += 1;
+            }
+        }
+        const bool use_pairs = sym.BN <= 256 && tc_pair_smem_bytes(sym.BN) <= 227 * 1024;
+        sym.npairs = use_pairs ? static_cast<int>(pr.size()) : 0;
+        if (use_pairs) sym.pairs.upload(pr.data(), pr.size(), stream);
+        encode_f32_map(&sym.tmA, sym.X32.ptr, sym.KP, B_pad, static_cast<uint32_t>(kTcBM), sym.LD);
+        encode_f32_map(&sym.tmB, sym.d32.ptr, sym.KP, static_cast<uint64_t>(2) * sym.NP, static_cast<uint32_t>(sym.BN), sym.KP);
+        CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
+        CK(cudaFuncSetAttribute(tc_local_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_pair_smem_bytes(256)));
+    }
+
+    // fp32 2-D tensor map: [rows][cols] with a row stride, {32 x box_rows} boxes, 128-byte swizzle
+    static void encode_f32_map(CUtensorMap *m, void *ptr, int cols, uint64_t rows_, uint32_t box_rows, int row_stride) {
+        using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                      const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        static EncodeFn encode = [] {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<EncodeFn>(fn);
+        }();
+        if (!encode) throw StatusError(TSV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), rows_};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride) * sizeof(float)};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kTcBK), box_rows};
+        const cuuint32_t estr[2] = {1, 1};
+        if (encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            throw StatusError(TSV_ECUDA, "tensor map encoding failed");
     }
 
     // Stream-K boundaries for K1: split the linear (tile, k-chunk) space into
@@ -1666,6 +1856,79 @@ struct tsv_ctx {
         CK(cudaGetLastError());
     }
 
+    // Forward / backward Walsh-Hadamard pass over a whole operand panel.
+    void launch_sym_panel(int dir, const double *in, double *out, bool with32, const int *done) {
+        const RomHost &mt = rom[sym.tab_kind];
+        SymPanelParams sp{};
+        sp.in = in;
+        sp.out = out;
+        sp.ld_in = static_cast<long long>(dir == 0 ? ldk : static_cast<size_t>(sym.lds));
+        sp.ld_out = static_cast<long long>(dir == 0 ? static_cast<size_t>(sym.lds) : ldk);
+        sp.rows = static_cast<int>(B_pad);
+        sp.n_plain = static_cast<int>(ldk);
+        sp.n_seg = sym.lds;
+        sp.src = mt.d_ssrc.ptr;
+        sp.dst = mt.d_sdst.ptr;
+        sp.n_orbits = mt.sred.n_orbits;
+        sp.n_valid = static_cast<int>(n);
+        sp.ld32 = static_cast<long long>(sym.LD);
+        sp.done = done;
+        if (with32) {
+            if (dir == 0) sp.x32 = sym.X32.ptr;
+            else sp.c32 = sym.Yc32.ptr;
+            sp.c_scale = sym.c_scale;
+        }
+        const unsigned grid = static_cast<unsigned>(std::min<size_t>((B_pad + kSymWarps - 1) / kSymWarps, static_cast<size_t>(sm_count) * 2));
+        if (dir == 0) launch_pdl(sym_panel_kernel<0>, grid, 32 * kSymWarps, sym.panel_smem, stream, sp);
+        else launch_pdl(sym_panel_kernel<1>, grid, 32 * kSymWarps, sym.panel_smem, stream, sp);
+        ++launches;
+    }
+
+    // K1 on mirror-symmetric ROMs: X -> Xs (Walsh-Hadamard over the mirror
+    // orbits), 8 irrep GEMMs Ys_r = Xs_r K''_r^T (1/8 of the DMMA FLOPs), the
+    // rounding-level defect K_r - K_sym on tcgen05 (TF32), Ys -> Y.
+    void launch_k1_sym(const int *done) {
+        const RomHost &mt = rom[sym.tab_kind];
+        launch_sym_panel(0, X.ptr, sym.Xs.ptr, sym.corr, done);
+        GemmSegParams gp{};
+        gp.A = sym.Xs.ptr;
+        gp.lda = sym.lds;
+        gp.Bt[0] = (rom[0].set && rom[0].sym ? rom[0] : rom[1]).d_ks.ptr;
+        gp.Bt[1] = (rom[1].set && rom[1].sym ? rom[1] : rom[0]).d_ks.ptr;
+        gp.tile_kind = tile_kind_d.ptr;
+        gp.C = sym.Ys.ptr;
+        gp.ldc = sym.lds;
+        gp.m_tiles = static_cast<int>(m_tiles);
+        gp.tiles_per_m = mt.k1_tiles_per_m;
+        gp.n_segs = static_cast<int>(mt.k1_segs.size());
+        gp.segs = mt.d_k1_segs.ptr;
+        gp.done = done;
+        gp.tile_counter = tile_counter.ptr;
+        gp.m_major = 1;
+        launch_pdl(gemm_seg_f64<K1Cfg>, std::min(k1_grid, gp.m_tiles * gp.tiles_per_m), K1Cfg::THREADS, K1Cfg::SMEM, stream, gp);
+        ++launches;
+        if (sym.corr) {
+            TcLocalParams tp{};
+            tp.tile_type = sym.tile_type.ptr;
+            tp.NP = sym.NP;
+            tp.BN = sym.BN;
+            tp.k_blocks = sym.KP / kTcBK;
+            tp.ZL = sym.Yc32.ptr;
+            tp.ldz = static_cast<long long>(sym.LD);
+            tp.done = done ? done : zero_flag.ptr;
+            if (sym.npairs)
+                launch_pdl(tc_local_pair_kernel, dim3(static_cast<unsigned>(sym.ntn), static_cast<unsigned>(sym.npairs)),
+                           kTcThreads, tc_pair_smem_bytes(sym.BN), stream, sym.tmA, sym.tmB, tp,
+                           static_cast<const int2 *>(sym.pairs.ptr));
+            else
+                launch_pdl(tc_local_tf32_kernel, dim3(static_cast<unsigned>(sym.ntn), static_cast<unsigned>(m_tiles)),
+                           kTcThreads, tc_smem_bytes(sym.BN), stream, sym.tmA, sym.tmB, tp);
+            ++launches;
+        }
+        launch_sym_panel(1, sym.Ys.ptr, Y.ptr, sym.corr, done);
+        CK(cudaGetLastError());
+    }
+
     void launch_k1(const int *done) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(stream, &cs));
@@ -1674,6 +1937,7 @@ struct tsv_ctx {
         const bool verify_mode = oz_s && oz_verify_digits();
         const bool hybrid = verify_mode && done;
         if (oz_s && !verify_mode) return oz_s == 9 ? launch_k1_oz<9>(done) : launch_k1_oz<10>(done);
+        if (sym.k1 && !oz_s) return launch_k1_sym(done);
         GemmParams gp = k1_params(done);
         if (hybrid) gp.skip_flag = yx;
         if (k1_small) {
@@ -2081,7 +2345,40 @@ struct tsv_ctx {
         gp.tile_counter = tile_counter.ptr;
         gp.n_major = 1;
         gp.col_map = mk.n_dense < mk.n_fine ? mk.d_dmap.ptr : nullptr;
-        if (mk.n_dense) {
+        if (mk.n_dense && sym.on && mk.sym) {
+            // mirror-symmetric ROM: 8 irrep GEMMs on the segmented Q panel
+            // (recover_range built it), then the inverse transform over the
+            // fine-DoF orbits scatters the dense rows into U
+            GemmSegParams sg{};
+            sg.A = sym.Xs.ptr + t * kBM * static_cast<size_t>(sym.lds);
+            sg.lda = sym.lds;
+            sg.Bt[0] = sg.Bt[1] = mk.d_phis.ptr;
+            sg.tile_kind = nullptr;
+            sg.C = sym.Us.ptr;
+            sg.ldc = mk.sfine.ld;
+            sg.m_tiles = static_cast<int>(t1 - t);
+            sg.tiles_per_m = mk.k6_tiles_per_m;
+            sg.n_segs = static_cast<int>(mk.k6_segs.size());
+            sg.segs = mk.d_k6_segs.ptr;
+            sg.row_scale = row_dt_d.ptr + t * kBM;
+            sg.col_bias[0] = sg.col_bias[1] = mk.d_uts.ptr;
+            sg.done = nullptr;
+            sg.tile_counter = tile_counter.ptr;
+            sg.m_major = 0;
+            gemm_seg_f64<K6Cfg><<<std::min(k6_grid, sg.m_tiles * sg.tiles_per_m), K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(sg);
+            SymFineParams fp{};
+            fp.Us = sym.Us.ptr;
+            fp.ldus = mk.sfine.ld;
+            fp.U = Uout;
+            fp.ldu = static_cast<long long>(ldu);
+            fp.rows = static_cast<int>((t1 - t) * kBM);
+            fp.src = mk.d_fsrc.ptr;
+            fp.dst = mk.d_fdst.ptr;
+            fp.n_orbits = mk.sfine.n_orbits;
+            dim3 fgrid(static_cast<unsigned>((fp.n_orbits + 255) / 256), static_cast<unsigned>((fp.rows + kFineRows - 1) / kFineRows));
+            sym_fine_kernel<<<fgrid, 256, 0, stream>>>(fp);
+            launches += 2;
+        } else if (mk.n_dense) {
             gemm_nt_f64<K6Cfg><<<std::min(k6_grid, gp.m_tiles * gp.n_tiles), K6Cfg::THREADS, K6Cfg::SMEM, stream>>>(gp);
             ++launches;
         }
@@ -2142,6 +2439,13 @@ struct tsv_ctx {
         for (size_t c = c0; c < c1; ++c) need[cell_row[c] / kBM] = 1;
         const size_t chunk_tiles = std::max<size_t>(1, std::min<size_t>(32, (size_t(1) << 30) / (ldu * 8 * kBM)));
         U.alloc(chunk_tiles * kBM * ldu);
+        if (sym.on) {
+            size_t ldus = 0;
+            for (int k = 0; k < 2; ++k)
+                if (rom[k].set && rom[k].sym) ldus = std::max<size_t>(ldus, static_cast<size_t>(rom[k].sfine.ld));
+            sym.Us.alloc(chunk_tiles * kBM * ldus);
+            launch_sym_panel(0, X.ptr, sym.Xs.ptr, false, nullptr);
+        }
         StressParams sp{};
         sp.ldu = static_cast<long long>(ldu);
         sp.row_cell = row_cell_d.ptr;
@@ -2383,6 +2687,8 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         CK(cudaMemset(ctx->tile_counter.ptr, 0, 2 * sizeof(unsigned)));
         ctx->state.alloc(1);
         CK(cudaMemset(ctx->state.ptr, 0, sizeof(CgState)));
+        ctx->zero_flag.alloc(1);
+        CK(cudaMemset(ctx->zero_flag.ptr, 0, sizeof(int)));
         return TSV_OK;
     });
     if (rc != TSV_OK) return rc;
@@ -2569,6 +2875,16 @@ int tsv_set_rom(tsv_ctx *ctx, int kind, const tsv_rom_desc *d) {
             }
             if (m.n_dense == n_fine) m.d_dmap.release();
             CK(cudaStreamSynchronize(ctx->stream));
+            {
+                PhaseTimer pts("  rom symmetry");
+                std::vector<double> kpu(n * n);
+                for (size_t a = 0; a < n; ++a)
+                    for (size_t k = 0; k < n; ++k) kpu[pidx(a, nn) * n + pidx(k, nn)] = d->a_element[a * n + k];
+                build_rom_symmetry(m, kpu, d->basis, d->thermal, dmap, ctx->stream, kBN, kKC);
+                if (tsv_ctx::getenv_flag("TSV_TIMING"))
+                    std::fprintf(stderr, "[tsv] rom kind %d: mirror symmetry %s (defect K %.2e, Phi %.2e)\n", kind,
+                                 m.sym ? "on" : "off", m.sym_defect_k, m.sym_defect_phi);
+            }
         }
         std::vector<double> hinv;
         for (int a = 0; a < 3; ++a)
@@ -2904,6 +3220,10 @@ int tsv_block_field(tsv_ctx *ctx, uint64_t cell, double *out) {
         const size_t ldu = round_up(mk.n_fine, 8);
         ctx->launch_scatter(ctx->x.ptr, 1);
         ctx->U.alloc(std::max(ctx->U.count, kBM * ldu));
+        if (ctx->sym.on) {
+            ctx->sym.Us.alloc(std::max(ctx->sym.Us.count, kBM * static_cast<size_t>(mk.sfine.ld)));
+            ctx->launch_sym_panel(0, ctx->X.ptr, ctx->sym.Xs.ptr, false, nullptr);
+        }
         ctx->launch_k6(mk, t, t + 1, ctx->U.ptr, ldu);
         CK(cudaMemcpyAsync(out, ctx->U.ptr + (j - t * kBM) * ldu, mk.n_fine * sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -2926,6 +3246,24 @@ int tsv_profile_apply(tsv_ctx *ctx, int reps, double *ms_per_launch) {
         CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         ctx->last_apply_ms = ms / reps;
         if (ms_per_launch) *ms_per_launch = ctx->last_apply_ms;
+        return TSV_OK;
+    });
+}
+
+int tsv_get_symmetry(tsv_ctx *ctx, tsv_symmetry_info *out) {
+    return guarded(ctx, [&] {
+        if (!out) throw StatusError(TSV_EINVAL, "get_symmetry: null output");
+        if (!ctx->layout_set) throw StatusError(TSV_ESTATE, "get_symmetry: no layout set");
+        std::memset(out, 0, sizeof *out);
+        out->recovery_symmetric = ctx->sym.on;
+        out->operator_symmetric = ctx->sym.k1;
+        out->defect_correction = ctx->sym.corr;
+        for (int k = 0; k < 2; ++k) {
+            out->defect_k[k] = ctx->rom[k].set ? ctx->rom[k].sym_defect_k : 0.0;
+            out->defect_phi[k] = ctx->rom[k].set ? ctx->rom[k].sym_defect_phi : 0.0;
+        }
+        if (ctx->sym.on)
+            for (int r = 0; r < 8; ++r) out->irrep_dofs[r] = ctx->rom[ctx->sym.tab_kind].sred.count[r];
         return TSV_OK;
     });
 }

@@ -133,20 +133,18 @@ __device__ __forceinline__ void mma_chunk_partial(double (&acc)[Cfg::FM][Cfg::FN
     }
 }
 
-// One tile segment: accumulate k-chunks [kc0, kc1) of tile (mt, nt).
+// Accumulate k-chunks [kc0, kc1) of one tile: A0 / B0 point at the tile's
+// first row (k = 0) of the operand panel / the matrix.
 template <class Cfg>
-__device__ __forceinline__ void gemm_segment(const GemmParams &p, double *As, double *Bs, int mt, int nt, int kc0,
-                                             int kc1, int fn_lim, double (&acc)[Cfg::FM][Cfg::FN][2]) {
+__device__ __forceinline__ void gemm_core(double *As, double *Bs, const double *A0, long long lda, const double *B0,
+                                          long long ldb, int kc0, int kc1, int fn_lim,
+                                          double (&acc)[Cfg::FM][Cfg::FN][2]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp / Cfg::WN, wn = warp % Cfg::WN;
-    const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
-    const double *A0 = p.A + static_cast<long long>(mt) * Cfg::BM * p.lda;
-    const double *Bbase = p.Bt_tab ? p.Bt_tab[p.tile_type[mt]] : (kind ? p.Bt[1] : p.Bt[0]);
-    const double *B0 = Bbase + static_cast<long long>(nt) * Cfg::BN * p.ldb;
 #pragma unroll
     for (int s = 0; s < Cfg::STAGES - 1; ++s) {
         if (kc0 + s < kc1)
-            gemm_load_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, kc0 + s);
+            gemm_load_stage<Cfg>(As + s * Cfg::A_STAGE, Bs + s * Cfg::B_STAGE, A0, lda, B0, ldb, kc0 + s);
         cp_async_commit();
     }
     for (int kc = kc0; kc < kc1; ++kc) {
@@ -156,7 +154,7 @@ __device__ __forceinline__ void gemm_segment(const GemmParams &p, double *As, do
         const int nk = kc + Cfg::STAGES - 1;
         if (nk < kc1) {
             const int st = (i + Cfg::STAGES - 1) % Cfg::STAGES;
-            gemm_load_stage<Cfg>(As + st * Cfg::A_STAGE, Bs + st * Cfg::B_STAGE, A0, p.lda, B0, p.ldb, nk);
+            gemm_load_stage<Cfg>(As + st * Cfg::A_STAGE, Bs + st * Cfg::B_STAGE, A0, lda, B0, ldb, nk);
         }
         cp_async_commit();
         const double *as = As + (i % Cfg::STAGES) * Cfg::A_STAGE + (wm * Cfg::TM + (lane >> 2)) * Cfg::SP + (lane & 3);
@@ -168,6 +166,17 @@ __device__ __forceinline__ void gemm_segment(const GemmParams &p, double *As, do
     }
     cp_async_wait<0>();
     __syncthreads();
+}
+
+// One tile segment: accumulate k-chunks [kc0, kc1) of tile (mt, nt).
+template <class Cfg>
+__device__ __forceinline__ void gemm_segment(const GemmParams &p, double *As, double *Bs, int mt, int nt, int kc0,
+                                             int kc1, int fn_lim, double (&acc)[Cfg::FM][Cfg::FN][2]) {
+    const int kind = p.tile_kind ? p.tile_kind[mt] : 0;
+    const double *A0 = p.A + static_cast<long long>(mt) * Cfg::BM * p.lda;
+    const double *Bbase = p.Bt_tab ? p.Bt_tab[p.tile_type[mt]] : (kind ? p.Bt[1] : p.Bt[0]);
+    const double *B0 = Bbase + static_cast<long long>(nt) * Cfg::BN * p.ldb;
+    gemm_core<Cfg>(As, Bs, A0, p.lda, B0, p.ldb, kc0, kc1, fn_lim, acc);
 }
 
 // Epilogue: lane holds C[row][col], C[row][col+1] (+ row_scale * col_bias).

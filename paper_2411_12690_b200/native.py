@@ -18,7 +18,7 @@ EXPORTS = [
     "tsv_ctx_create", "tsv_ctx_destroy", "tsv_last_error", "tsv_abi_version", "tsv_set_rom", "tsv_set_layout", "tsv_set_delta_t",
     "tsv_set_dirichlet", "tsv_set_bc", "tsv_index_global_nodes", "tsv_get_index", "tsv_get_dof_map", "tsv_get_lattice",
     "tsv_get_constrained", "tsv_get_load", "tsv_apply", "tsv_precond_apply", "tsv_precond_setup", "tsv_debug_coarse", "tsv_solve", "tsv_set_solution", "tsv_recover",
-    "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing",
+    "tsv_recover_resident", "tsv_copy_stress", "tsv_cutplane", "tsv_block_field", "tsv_profile_apply", "tsv_get_timing", "tsv_get_symmetry",
     "tsv_rom_dims", "tsv_rom_fingerprint", "tsv_rom_file_info", "tsv_build_rom", "tsv_load_rom_file", "tsv_save_rom_file", "tsv_host_register", "tsv_host_unregister", "tsv_host_alloc", "tsv_host_free", "tsv_fp64_peak",
 ]
 
@@ -70,6 +70,11 @@ class Timing(C.Structure):
                 ("kernel_launches", C.c_uint64)]
 
 
+class SymmetryInfo(C.Structure):
+    _fields_ = [("recovery_symmetric", C.c_int), ("operator_symmetric", C.c_int), ("defect_correction", C.c_int),
+                ("irrep_dofs", C.c_int * 8), ("defect_k", C.c_double * 2), ("defect_phi", C.c_double * 2)]
+
+
 _lib = None
 
 
@@ -114,6 +119,7 @@ def load(path: str = LIB_PATH):
         "tsv_block_field": (i, [vp, u64, vp]),
         "tsv_profile_apply": (i, [vp, i, P(d)]),
         "tsv_get_timing": (i, [vp, P(Timing)]),
+        "tsv_get_symmetry": (i, [vp, P(SymmetryInfo)]),
         "tsv_host_register": (i, [vp, sz]),
         "tsv_host_unregister": (i, [vp]),
         "tsv_host_alloc": (i, [sz, C.POINTER(vp)]),
