@@ -252,10 +252,14 @@ int tsv_get_timing(tsv_ctx *ctx, tsv_timing *out);
 /* Mirror symmetry of the loaded ROMs (csrc/symmetry.hpp). A macro-element
  * whose grid and materials are symmetric about its three mid-planes has
  * K_r and Phi block diagonal over the 8 irreps of Z2^3; tsv_set_rom checks
- * that numerically and the layout then runs K1 / K6 as 8 irrep GEMMs with
- * 1/8 of the FP64 FLOPs (the rounding-level defect K_r - K_sym is added back
- * on the tensor cores, so the operator stays the reference's K_r).
- * TSV_SYM=0 disables the path. */
+ * that numerically and the layout then runs K1 / K6 as 8 irrep products
+ * with 1/8 of the FP64 FLOPs. K1 is one fused kernel (rows of the operand
+ * panel in shared memory, butterflies in place, the irrep blocks on the DMMA
+ * pipe); inside the PCG loop the A x of the true-residual check stays on the
+ * reference's K_r (exact int8 product), so the returned solution satisfies
+ * the reference's stopping rule for the reference's operator.
+ * TSV_SYM=0 disables the path; TSV_SYM_K1_FUSED=0 selects the multi-kernel
+ * K1 (panel passes + segmented GEMM + TF32 term for K_r - K_sym). */
 typedef struct tsv_symmetry_info {
     int recovery_symmetric;   /* K6 on the irrep path for this layout */
     int operator_symmetric;   /* K1 on the irrep path for this layout */
@@ -263,6 +267,8 @@ typedef struct tsv_symmetry_info {
     int irrep_dofs[8];        /* reduced DoFs per irrep */
     double defect_k[2];       /* per kind: max off-block |K''| / max |K''| */
     double defect_phi[2];
+    int operator_fused;       /* K1 irrep path as one fused kernel */
+    int reserved_;
 } tsv_symmetry_info;
 int tsv_get_symmetry(tsv_ctx *ctx, tsv_symmetry_info *out);
 

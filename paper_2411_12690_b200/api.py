@@ -338,7 +338,7 @@ class GpuGlobalStage:
         t = native.SymmetryInfo()
         self._check(self._L.tsv_get_symmetry(self._h, C.byref(t)))
         return dict(recovery=bool(t.recovery_symmetric), operator=bool(t.operator_symmetric),
-                    correction=bool(t.defect_correction), irrep_dofs=list(t.irrep_dofs),
+                    correction=bool(t.defect_correction), fused=bool(t.operator_fused), irrep_dofs=list(t.irrep_dofs),
                     defect_k=list(t.defect_k), defect_phi=list(t.defect_phi))
 
     def timing(self) -> Timing:

@@ -201,6 +201,8 @@ struct RomHost {
     DevBuf<short> d_ssrc, d_sdst;         // reduced orbit tables
     DevBuf<int> d_fsrc, d_fdst;           // fine orbit tables (U column / Us column)
     DevBuf<GemmSeg> d_k1_segs, d_k6_segs;
+    SymK1Pack k1f;                        // fused K1 (sym_k1_fused_kernel): items, column lists
+    DevBuf<double> d_kf;                  // K'' in DMMA fragment order
     // K_r - K_sym (the rounding-level symmetry defect of K_r), TF32, times 2^d_exp:
     // added back on the tensor cores so the operator stays the reference's K_r
     std::vector<float> d32_host;          // [n][n] panel order, scaled
@@ -221,6 +223,8 @@ void build_rom_symmetry(RomHost &m, const std::vector<double> &kp, const double 
     m.sym_defect_k = pk.defect_k;
     m.sym_defect_phi = pk.defect_phi;
     if (!ok) return;
+    m.k1f.build(pk.red, pk.k1_segs, pk.ks, kSymKB);
+    m.d_kf.upload(m.k1f.bf.data(), m.k1f.bf.size(), stream);
     m.sred = std::move(pk.red);
     m.sfine = std::move(pk.fine);
     m.k1_segs = std::move(pk.k1_segs);
@@ -333,6 +337,13 @@ struct tsv_ctx {
         int lds = 0;       // row length of the segmented reduced panel
         size_t panel_smem = 0;
         DevBuf<double> Xs, Ys, Us;
+        // fused K1 (one kernel, sym_k1_fused_kernel)
+        bool fused = false;
+        int f_mf = 2, f_items = 0, f_rounds = 0, f_tiles = 0, f_coltab = 0, f_grid = 0;
+        size_t f_smem = 0;
+        DevBuf<int4> f_tile_tab;
+        DevBuf<SymK1Item> f_item_tab;
+        DevBuf<short> f_col_tab;
         // K_r symmetry-defect correction on tcgen05 (TF32): Yc32 = X32 D32^T
         bool corr = false;
         int KP = 0, NP = 0, BN = 0, ntn = 0, LD = 0, npairs = 0;
@@ -542,7 +553,7 @@ struct tsv_ctx {
     // Mirror-symmetric path (sym.cuh): on when every ROM the layout uses passed
     // the symmetry check in tsv_set_rom and the kinds share the reduced tables.
     void setup_symmetry(const bool need[2]) {
-        sym.on = sym.k1 = sym.corr = false;
+        sym.on = sym.k1 = sym.corr = sym.fused = false;
         const RomHost *first = nullptr;
         for (int k = 0; k < 2; ++k) {
             if (!need[k]) continue;
@@ -568,6 +579,8 @@ struct tsv_ctx {
         const char *env = std::getenv("TSV_SYM_K1");
         sym.k1 = env ? *env == '1' : !k1_small;  // TSV_SYM_K1=1 forces it on small arrays too (tests)
         if (!sym.k1) return;
+        setup_sym_fused(*first);
+        if (sym.fused) return;
         sym.Ys.alloc(B_pad * static_cast<size_t>(sym.lds));
         CK(cudaMemsetAsync(sym.Ys.ptr, 0, sym.Ys.count * sizeof(double), stream));
         // correction operand: D32[kind][NP][KP] (the tc_local layout), one common scale
@@ -631,6 +644,100 @@ struct tsv_ctx {
         encode_f32_map(&sym.tmB, sym.d32.ptr, sym.KP, static_cast<uint64_t>(2) * sym.NP, static_cast<uint32_t>(sym.BN), sym.KP);
         CK(cudaFuncSetAttribute(tc_local_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes(256)));
         CK(cudaFuncSetAttribute(tc_local_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_pair_smem_bytes(256)));
+    }
+
+    // Fused K1 on mirror-symmetric ROMs (sym_k1_fused_kernel): item / column /
+    // tile tables. TSV_SYM_K1_FUSED=0 keeps the multi-kernel path (panel
+    // passes + segmented GEMM); TSV_SYM_K1_MF=2|3|4 picks 16 / 24 / 32 rows per CTA.
+    template <int MF, int WARPS, int MINB>
+    bool sym_fused_config() {
+        auto kern = sym_k1_fused_kernel<MF, WARPS, MINB>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sym.f_smem)) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, sym.f_smem));
+        if (occ < 1) return false;
+        sym.f_grid = std::min(sym.f_tiles, occ * sm_count);
+        return true;
+    }
+
+    void setup_sym_fused(const RomHost &first) {
+        sym.fused = false;
+        const char *env = std::getenv("TSV_SYM_K1_FUSED");
+        if (env && *env == '0') return;
+        const char *emf = std::getenv("TSV_SYM_K1_MF");
+        const int mf = emf ? std::atoi(emf) : 2;
+        if (mf < 2 || mf > 4) return;
+        const int warps = mf == 2 ? 8 : 16;
+        const SymK1Pack &pk = first.k1f;
+        std::vector<short> flush;
+        if (pk.items.empty() || pk.flush_rounds(warps, flush) > kSymSlots - 1) return;
+        std::vector<SymK1Item> items(pk.items.size());
+        for (size_t i = 0; i < items.size(); ++i) {
+            SymK1Item it{};
+            it.b_off = pk.items[i].b_off;
+            it.ksteps = pk.items[i].ksteps;
+            it.ksteps4 = pk.items[i].ksteps4;
+            it.kcol = pk.items[i].kcol;
+            it.ncol = pk.items[i].ncol;
+            it.nvalid = pk.items[i].nvalid;
+            it.flush_round = flush[i];
+            items[i] = it;
+        }
+        sym.f_mf = mf;
+        sym.f_items = static_cast<int>(items.size());
+        sym.f_rounds = (sym.f_items + warps - 1) / warps;
+        sym.f_coltab = static_cast<int>(pk.coltab.size());
+        sym.f_smem = sym_k1_smem(mf, static_cast<int>(ldk), first.sred.n_orbits, sym.f_coltab, sym.f_items);
+        if (sym.f_smem > 227 * 1024) return;
+        // row tiles: runs of same-kind M tiles cut into 8 MF rows
+        std::vector<int4> tiles;
+        const int R = 8 * mf;
+        for (size_t t = 0; t < tile_kind.size();) {
+            size_t e = t;
+            while (e < tile_kind.size() && tile_kind[e] == tile_kind[t]) ++e;
+            const int r0 = static_cast<int>(t * kBM), r1 = static_cast<int>(e * kBM);
+            for (int r = r0; r < r1; r += R) tiles.push_back(make_int4(r, std::min(R, r1 - r), tile_kind[t], 0));
+            t = e;
+        }
+        sym.f_tiles = static_cast<int>(tiles.size());
+        const bool ok = mf == 2 ? sym_fused_config<2, 8, 2>() : mf == 3 ? sym_fused_config<3, 16, 1>() : sym_fused_config<4, 16, 1>();
+        if (!ok) return;
+        sym.f_tile_tab.upload(tiles.data(), tiles.size(), stream);
+        sym.f_item_tab.upload(items.data(), items.size(), stream);
+        sym.f_col_tab.upload(pk.coltab.data(), pk.coltab.size(), stream);
+        CK(cudaStreamSynchronize(stream));
+        sym.fused = true;
+    }
+
+    void launch_k1_sym_fused(const int *done, const int *skip) {
+        const RomHost &mt = rom[sym.tab_kind];
+        SymK1Params sp{};
+        sp.X = X.ptr;
+        sp.Y = Y.ptr;
+        sp.ld = static_cast<long long>(ldk);
+        sp.ldk = static_cast<int>(ldk);
+        sp.tiles = sym.f_tile_tab.ptr;
+        sp.n_tiles = sym.f_tiles;
+        sp.Bf[0] = (rom[0].set && rom[0].sym ? rom[0] : rom[1]).d_kf.ptr;
+        sp.Bf[1] = (rom[1].set && rom[1].sym ? rom[1] : rom[0]).d_kf.ptr;
+        sp.items = sym.f_item_tab.ptr;
+        sp.n_items = sym.f_items;
+        sp.rounds = sym.f_rounds;
+        sp.orb = mt.d_ssrc.ptr;
+        sp.n_orbits = mt.sred.n_orbits;
+        sp.coltab = sym.f_col_tab.ptr;
+        sp.n_coltab = sym.f_coltab;
+        sp.done = done;
+        sp.skip_flag = skip;
+        sp.tile_counter = tile_counter.ptr;
+        if (sym.f_mf == 2) launch_pdl(sym_k1_fused_kernel<2, 8, 2>, sym.f_grid, 256, sym.f_smem, stream, sp);
+        else if (sym.f_mf == 3) launch_pdl(sym_k1_fused_kernel<3, 16, 1>, sym.f_grid, 512, sym.f_smem, stream, sp);
+        else launch_pdl(sym_k1_fused_kernel<4, 16, 1>, sym.f_grid, 512, sym.f_smem, stream, sp);
+        ++launches;
+        CK(cudaGetLastError());
     }
 
     // fp32 2-D tensor map: [rows][cols] with a row stride, {32 x box_rows} boxes, 128-byte swizzle
@@ -1749,6 +1856,12 @@ struct tsv_ctx {
             const int s = std::atoi(v);
             return (s == 9 || s == 10) ? s : 0;
         }
+        // With the irrep K1 (mirror-symmetric ROMs) the A x of the check runs on the
+        // exact int8 path: the irrep products round differently from the plain
+        // DMMA product, and at config 3 the FP64 rounding of A x on the smooth
+        // solution is already ~tol |b| (sym vs plain: 1.1e-12 |b|), so an FP64
+        // check on that path never passes (B200: 84 restarts in 400 iterations).
+        if (sym.k1 && sym.fused && ldk <= 1024) return 10;
         // Default off since round 2: with the s = 2 coarse space the FP64 DMMA
         // check restarts no more often than the exact int8 one (config 3: 57
         // iterations / 1 restart either way; configs 0-4 unchanged), and the two
@@ -1937,8 +2050,21 @@ struct tsv_ctx {
         const bool verify_mode = oz_s && oz_verify_digits();
         const bool hybrid = verify_mode && done;
         if (oz_s && !verify_mode) return oz_s == 9 ? launch_k1_oz<9>(done) : launch_k1_oz<10>(done);
-        if (sym.k1 && !oz_s) return launch_k1_sym(done);
+        if (sym.k1 && !sym.fused && !oz_s) return launch_k1_sym(done);
         GemmParams gp = k1_params(done);
+        if (sym.k1 && sym.fused) {
+            // The irrep products carry the iteration; inside the PCG loop the A x of
+            // the true-residual check goes to the exact int8 path (hybrid) or, when
+            // that is off, to the plain DMMA K1 below (run only when y_holds_x).
+            launch_k1_sym_fused(done, yx);
+            if (!done) return;
+            if (hybrid) {
+                if (oz_s == 9) launch_k1_oz<9>(done, yx);
+                else launch_k1_oz<10>(done, yx);
+                return;
+            }
+            gp.run_flag = yx;
+        }
         if (hybrid) gp.skip_flag = yx;
         if (k1_small) {
             gp.m_tiles = static_cast<int>(B_pad / K1SmallCfg::BM);
@@ -2019,7 +2145,10 @@ struct tsv_ctx {
 
     int graph_kernels_per_iteration() const {
         const int schwarz = as_split() ? (fused_gu() ? 10 : 11) : (fused_gu() ? 9 : 10);
-        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? schwarz : 4) + (oz_s ? (oz_verify_digits() ? 2 : 1) : 0);
+        const bool oz_verify = oz_s && oz_verify_digits();
+        int symk = 0;  // extra launches of the irrep K1
+        if (sym.k1 && !(oz_s && !oz_verify)) symk = sym.fused ? (oz_verify ? 0 : 1) : (sym.corr ? 3 : 2);
+        return (pre_kind == TSV_PRECOND_SCHWARZ2 ? schwarz : 4) + (oz_s ? (oz_verify ? 2 : 1) : 0) + symk;
     }
 
     // Split Schwarz loop (opt-in, TSV_AS_SPLIT=1): after r is updated, the
@@ -3258,6 +3387,7 @@ int tsv_get_symmetry(tsv_ctx *ctx, tsv_symmetry_info *out) {
         out->recovery_symmetric = ctx->sym.on;
         out->operator_symmetric = ctx->sym.k1;
         out->defect_correction = ctx->sym.corr;
+        out->operator_fused = ctx->sym.k1 && ctx->sym.fused;
         for (int k = 0; k < 2; ++k) {
             out->defect_k[k] = ctx->rom[k].set ? ctx->rom[k].sym_defect_k : 0.0;
             out->defect_phi[k] = ctx->rom[k].set ? ctx->rom[k].sym_defect_phi : 0.0;

@@ -47,6 +47,7 @@ struct GemmParams {
     const double *col_bias[2];   // u_T per kind
     const int *done;             // nullable: early exit when *done != 0
     const int *skip_flag;        // nullable: early exit when *skip_flag != 0 (hybrid K1: A x goes to int8)
+    const int *run_flag;         // nullable: early exit when *run_flag == 0 (the A x products of a symmetric K1)
     unsigned *tile_counter;      // [2] {next tile, exited CTAs}, zero between launches
     int n_major;                 // tile order: 0 = M major (K1: A streamed once, K_r in L2),
                                  // 1 = N major (K6: Phi streamed once, the Q chunk in L2)
@@ -242,7 +243,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_nt_f64(GemmParam
     const int tid = threadIdx.x;
     const int total = p.m_tiles * p.n_tiles;
     const bool skip = (p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) ||
-                      (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0);
+                      (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0) ||
+                      (p.run_flag != nullptr && *reinterpret_cast<const volatile int *>(p.run_flag) == 0);
 
     while (!skip) {
         if (tid == 0) s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
@@ -293,7 +295,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_splitk_f64(GemmP
     constexpr int NACC = Cfg::FM * Cfg::FN * 2;
     const int tid = threadIdx.x;
     if ((p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) ||
-        (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0))
+        (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0) ||
+        (p.run_flag != nullptr && *reinterpret_cast<const volatile int *>(p.run_flag) == 0))
         return;
     const int S = sk.S;
     const int tile = blockIdx.x / S, s = blockIdx.x % S;
@@ -365,7 +368,9 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_streamk_f64(Gemm
     constexpr int NACC = Cfg::FM * Cfg::FN * 2;
     const int tid = threadIdx.x, g = blockIdx.x;
     if (p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) return;
-    if (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0) return;
+    if ((p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0) ||
+        (p.run_flag != nullptr && *reinterpret_cast<const volatile int *>(p.run_flag) == 0))
+        return;
     const int KC = p.k_chunks;
     const int i0 = sk.start[g], i1 = sk.start[g + 1];
     int it = i0;

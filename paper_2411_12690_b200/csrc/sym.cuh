@@ -263,4 +263,246 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_seg_f64(GemmSegP
     }
 }
 
+
+// ------------------------------------------------ fused K1 (one kernel)
+// Y = X K_r for a mirror-symmetric K_r, one pass over the panel: a CTA takes
+// R = 8 MF whole rows of X into shared memory (plain panel layout), runs the
+// Walsh-Hadamard butterflies over the mirror orbits in place (combination w
+// lands on member w), multiplies every irrep block on the DMMA pipe with the
+// A fragments gathered from shared memory through the irrep's column list and
+// the K''_r fragments streamed from L2 in fragment order, writes the products
+// back in place, runs the inverse butterflies and stores the rows. HBM
+// traffic is X in + Y out; FLOPs are 1/8 of the dense product.
+//
+// Work items are (irrep, pair of 8-column fragments); item i runs in round
+// i / WARPS on warp i % WARPS. The product of irrep r overwrites its own
+// operand columns, so an item's accumulators are parked in registers until
+// the round in which the last item of its irrep ran (flush_round; at most
+// kSymSlots - 1 rounds later - checked on the host).
+//
+// Shared-memory access: the row pitch is ldk + 4 doubles, so the A fragment
+// loads of a half-warp (4 rows x 4 k) are conflict-free when the four columns
+// of a k-step differ mod 4; the host orders each irrep's column list that way
+// (SymK1Pack). A lane's columns for four consecutive k-steps are one 8-byte
+// load from the transposed list [lane % 4][k-step].
+constexpr int kSymSlots = 2;
+constexpr int kSymKB = 4;  // k-steps (of 4) per K'' prefetch chunk
+
+struct SymK1Item {
+    int b_off;          // first double of the item's K'' fragments [ksteps4][2][32]
+    short ksteps;       // k-steps of 4 (even); the fragment array is padded to a multiple of kSymKB
+    short kcol;         // coltab offset of the irrep's transposed k column list [4][ksteps4]
+    short ncol;         // coltab offset of the first fragment's 8 output columns (the second follows)
+    short nvalid;       // valid output columns of the pair (1..16)
+    short flush_round;  // round after which the irrep's operand columns are dead
+    short ksteps4;      // ksteps rounded up to kSymKB
+};
+static_assert(sizeof(SymK1Item) == 16, "SymK1Item");
+
+struct SymK1Params {
+    const double *X;
+    double *Y;
+    long long ld;                // panel row pitch (ldk)
+    int ldk;                     // doubles per row copied in / out
+    const int4 *tiles;           // [n_tiles] {row0, rows (<= R, multiple of 8), kind, 0}
+    int n_tiles;
+    const double *Bf[2];         // per kind: K'' in fragment order
+    const SymK1Item *items;
+    int n_items, rounds;
+    const short *orb;            // [n_orbits][8] plain columns of the orbit members (-1: absent)
+    int n_orbits;
+    const short *coltab;
+    int n_coltab;
+    const int *done;             // nullable
+    const int *skip_flag;        // nullable: early exit when != 0 (A x goes to the verification path)
+    unsigned *tile_counter;
+};
+
+inline size_t sym_k1_smem(int mf, int ldk, int n_orbits, int n_coltab, int n_items) {
+    size_t b = static_cast<size_t>(mf) * 8 * (ldk + 4) * sizeof(double);
+    b += static_cast<size_t>(n_items) * sizeof(SymK1Item);
+    b += (static_cast<size_t>(n_orbits) * 8 + n_coltab) * sizeof(short);
+    return (b + 15) / 16 * 16;
+}
+
+// In-place butterflies over every (row, orbit) of the tile; INV: 1 / |orbit|.
+template <bool INV, int THREADS>
+__device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int R, const short *orb, int n_orbits) {
+    for (int t = threadIdx.x; t < R * n_orbits; t += THREADS) {
+        const int r = t / n_orbits, o = t - r * n_orbits;
+        const int4 mv = *reinterpret_cast<const int4 *>(orb + o * 8);
+        short m[8];
+        m[0] = static_cast<short>(mv.x), m[1] = static_cast<short>(mv.x >> 16);
+        m[2] = static_cast<short>(mv.y), m[3] = static_cast<short>(mv.y >> 16);
+        m[4] = static_cast<short>(mv.z), m[5] = static_cast<short>(mv.z >> 16);
+        m[6] = static_cast<short>(mv.w), m[7] = static_cast<short>(mv.w >> 16);
+        double *row = xs + r * P;
+        double x[8];
+        int f = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            x[g] = m[g] >= 0 ? row[m[g]] : 0.0;
+            if (m[g] >= 0) f |= g;
+        }
+        sym_butterfly(x, f);
+        const double s = !INV ? 1.0 : f == 7 ? 0.125 : (f == 0 ? 1.0 : ((f & (f - 1)) == 0 ? 0.5 : 0.25));
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+            if (m[g] >= 0) row[m[g]] = INV ? s * x[g] : x[g];
+    }
+}
+
+template <int MF, int WARPS, int MINB>
+__global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Params p) {
+    pdl_wait();
+    extern __shared__ __align__(16) double sym_smem[];
+    __shared__ int s_tile;
+    constexpr int R = 8 * MF, THREADS = 32 * WARPS;
+    const int P = p.ldk + 4;
+    double *xs = sym_smem;
+    SymK1Item *items = reinterpret_cast<SymK1Item *>(xs + static_cast<size_t>(R) * P);
+    short *orb = reinterpret_cast<short *>(items + p.n_items);
+    short *coltab = orb + p.n_orbits * 8;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool skip = (p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) ||
+                      (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0);
+    if (!skip) {
+        for (int i = tid; i < p.n_items * 4; i += THREADS)
+            reinterpret_cast<int *>(items)[i] = reinterpret_cast<const int *>(p.items)[i];
+        for (int i = tid; i < p.n_orbits * 8; i += THREADS) orb[i] = p.orb[i];
+        for (int i = tid; i < p.n_coltab; i += THREADS) coltab[i] = p.coltab[i];
+    }
+    const int cpr = p.ldk / 2;  // 16-byte chunks per row
+    while (!skip) {
+        if (tid == 0) s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile >= p.n_tiles) break;
+        const int4 tl = p.tiles[tile];
+        const int rows = tl.y;
+        const double *Bf = tl.z ? p.Bf[1] : p.Bf[0];
+        // ---- rows in (absent rows of a short tile: zeros)
+        {
+            const double *src = p.X + static_cast<long long>(tl.x) * p.ld;
+            for (int i = tid; i < R * cpr; i += THREADS) {
+                const int r = i / cpr, c = i - r * cpr;
+                if (r < rows) cp_async16(xs + r * P + 2 * c, src + r * p.ld + 2 * c);
+                else *reinterpret_cast<double2 *>(xs + r * P + 2 * c) = make_double2(0.0, 0.0);
+            }
+            cp_async_commit();
+        }
+        // the first K'' chunk of this warp's first item while the rows land
+        double bc[kSymKB][2], bn[kSymKB][2];
+        if (warp < p.n_items) {
+            const double *bp = Bf + items[warp].b_off + lane;
+#pragma unroll
+            for (int s = 0; s < kSymKB; ++s) {
+                bc[s][0] = __ldg(bp + (2 * s) * 32);
+                bc[s][1] = __ldg(bp + (2 * s + 1) * 32);
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+        sym_tile_butterflies<false, THREADS>(xs, P, R, orb, p.n_orbits);
+        __syncthreads();
+        // ---- irrep products
+        double acc[kSymSlots][MF][2][2];
+        int pend_round[kSymSlots], pend_ncol[kSymSlots], pend_nvalid[kSymSlots];
+#pragma unroll
+        for (int v = 0; v < kSymSlots; ++v) pend_round[v] = -1;
+        const double *arow = xs + (lane >> 2) * P;
+        for (int t0 = 0; t0 < p.rounds; t0 += kSymSlots) {
+#pragma unroll
+            for (int v = 0; v < kSymSlots; ++v) {
+                const int t = t0 + v;
+                const int it = t * WARPS + warp;
+                if (t < p.rounds && it < p.n_items) {
+                    const SymK1Item item = items[it];
+#pragma unroll
+                    for (int i = 0; i < MF; ++i) acc[v][i][0][0] = acc[v][i][0][1] = acc[v][i][1][0] = acc[v][i][1][1] = 0.0;
+                    const double *bp = Bf + item.b_off + lane;
+                    const short *kc = coltab + item.kcol + (lane & 3) * item.ksteps4;
+                    const int ks = item.ksteps;
+                    const bool more = it + WARPS < p.n_items;
+                    const double *bp_next = more ? Bf + items[it + WARPS].b_off + lane : bp;
+                    for (int s0 = 0; s0 < ks; s0 += kSymKB) {
+                        const bool last = s0 + kSymKB >= ks;
+                        if (!last || more) {
+                            const double *q = last ? bp_next : bp + (s0 + kSymKB) * 64;
+#pragma unroll
+                            for (int s = 0; s < kSymKB; ++s) {
+                                bn[s][0] = __ldg(q + (2 * s) * 32);
+                                bn[s][1] = __ldg(q + (2 * s + 1) * 32);
+                            }
+                        }
+                        const short4 cv = *reinterpret_cast<const short4 *>(kc + s0);
+                        const int cols[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+                        for (int s = 0; s < kSymKB; ++s) {
+                            if (s < 2 || s0 + s < ks) {  // ksteps is even: only the second half of a chunk can be absent
+                                double af[MF];
+#pragma unroll
+                                for (int i = 0; i < MF; ++i) af[i] = arow[i * 8 * P + cols[s]];
+#pragma unroll
+                                for (int i = 0; i < MF; ++i) {
+                                    dmma_8x8x4(acc[v][i][0][0], acc[v][i][0][1], af[i], bc[s][0]);
+                                    dmma_8x8x4(acc[v][i][1][0], acc[v][i][1][1], af[i], bc[s][1]);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int s = 0; s < kSymKB; ++s) bc[s][0] = bn[s][0], bc[s][1] = bn[s][1];
+                    }
+                    pend_round[v] = item.flush_round;
+                    pend_ncol[v] = item.ncol;
+                    pend_nvalid[v] = item.nvalid;
+                }
+                __syncthreads();  // round t done: operands of irreps that ended in it are dead
+                if (t < p.rounds) {
+#pragma unroll
+                    for (int w = 0; w < kSymSlots; ++w) {
+                        if (pend_round[w] >= 0 && pend_round[w] <= t) {
+                            double *orow = xs + (lane >> 2) * P;
+#pragma unroll
+                            for (int fr = 0; fr < 2; ++fr) {
+                                const int j = 8 * fr + 2 * (lane & 3);
+                                const short *nc = coltab + pend_ncol[w] + j;
+                                const int c0 = nc[0], c1 = nc[1];
+                                const bool v0 = j < pend_nvalid[w], v1 = j + 1 < pend_nvalid[w];
+#pragma unroll
+                                for (int i = 0; i < MF; ++i) {
+                                    if (v0) orow[i * 8 * P + c0] = acc[w][i][fr][0];
+                                    if (v1) orow[i * 8 * P + c1] = acc[w][i][fr][1];
+                                }
+                            }
+                            pend_round[w] = -1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        sym_tile_butterflies<true, THREADS>(xs, P, R, orb, p.n_orbits);
+        __syncthreads();
+        // ---- rows out
+        {
+            double *dst = p.Y + static_cast<long long>(tl.x) * p.ld;
+            for (int i = tid; i < rows * cpr; i += THREADS) {
+                const int r = i / cpr, c = i - r * cpr;
+                *reinterpret_cast<double2 *>(dst + r * p.ld + 2 * c) = *reinterpret_cast<const double2 *>(xs + r * P + 2 * c);
+            }
+        }
+        __syncthreads();
+    }
+    pdl_trigger();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&p.tile_counter[1], 1u) == gridDim.x - 1) {
+            p.tile_counter[0] = 0u;
+            p.tile_counter[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
 }  // namespace tsvb200

@@ -359,4 +359,126 @@ struct SymRomPack {
     }
 };
 
+
+// Host tables of the fused K1 kernel (sym.cuh: sym_k1_fused_kernel): work
+// items (irrep, pair of 8-column fragments) in irrep order, the irreps' column
+// lists in the plain panel layout, and K''_r in DMMA fragment order per item
+// ([k-step][fragment][lane]: B[n = 16 j + 8 f + lane / 4][k = 4 s + lane % 4],
+// zero padded to whole chunks of `kb` k-steps).
+//
+// The k order of an irrep is free (a permutation of its columns applied to
+// both operands): columns are dealt into k-steps so that the four columns of
+// a k-step differ mod 4 wherever the residue classes allow it, which makes
+// the kernel's A fragment loads (row pitch = 4 mod 16 doubles) conflict-free.
+struct SymK1Pack {
+    struct Item {
+        int b_off;
+        short ksteps, ksteps4, kcol, ncol, nvalid, irrep;
+    };
+    std::vector<Item> items;
+    std::vector<short> coltab;
+    std::vector<double> bf;
+    int conflict_quads = 0, quads = 0;  // k-steps whose columns collide mod 4 / all k-steps
+
+    // segs / ks: SymRomPack::k1_segs and ::ks of the same ROM (one segment per non-empty irrep, in irrep order)
+    void build(const SymTables &R, const std::vector<GemmSeg> &segs, const std::vector<double> &ks, int kb = 4) {
+        items.clear();
+        coltab.clear();
+        bf.clear();
+        conflict_quads = quads = 0;
+        size_t si = 0;
+        for (int r = 0; r < 8; ++r) {
+            std::vector<int> cols;  // ascending plain column = ascending index in the packed block
+            for (int d = 0; d < R.n; ++d)
+                if (R.label[d] == r) cols.push_back(d);
+            if (cols.empty()) continue;
+            const GemmSeg &g = segs[si++];
+            const int nr = static_cast<int>(cols.size());
+            const double *blk = ks.data() + g.b_off;
+            const int ksteps = (nr + 7) / 8 * 2;  // even
+            const int ksteps4 = (ksteps + kb - 1) / kb * kb;
+            // k order: korder[k] = index into cols (or -1: padding)
+            std::vector<int> korder(static_cast<size_t>(ksteps) * 4, -1);
+            {
+                std::vector<int> cls[4];
+                for (int i = nr - 1; i >= 0; --i) cls[cols[i] & 3].push_back(i);  // pop_back yields ascending
+                for (int s = 0; s < ksteps; ++s) {
+                    // one column from each of the (up to four) fullest classes
+                    int order[4] = {0, 1, 2, 3};
+                    std::sort(order, order + 4, [&](int a, int b) { return cls[a].size() > cls[b].size(); });
+                    int filled = 0;
+                    for (int c = 0; c < 4 && filled < 4; ++c)
+                        if (!cls[order[c]].empty()) {
+                            korder[s * 4 + filled++] = cls[order[c]].back();
+                            cls[order[c]].pop_back();
+                        }
+                    // classes exhausted unevenly: fill the k-step from the fullest remaining class
+                    while (filled < 4) {
+                        int best = 0;
+                        for (int c = 1; c < 4; ++c)
+                            if (cls[c].size() > cls[best].size()) best = c;
+                        if (cls[best].empty()) break;
+                        korder[s * 4 + filled++] = cls[best].back();
+                        cls[best].pop_back();
+                    }
+                }
+                for (int s = 0; s < ksteps; ++s) {
+                    bool clash = false;
+                    for (int a = 0; a < 4; ++a)
+                        for (int b = a + 1; b < 4; ++b)
+                            if (korder[s * 4 + a] >= 0 && korder[s * 4 + b] >= 0 &&
+                                ((cols[korder[s * 4 + a]] ^ cols[korder[s * 4 + b]]) & 3) == 0)
+                                clash = true;
+                    conflict_quads += clash;
+                    ++quads;
+                }
+            }
+            while (coltab.size() % 4) coltab.push_back(0);
+            const int koff = static_cast<int>(coltab.size());
+            // transposed k column list [4][ksteps4]; padding points at a real column (its K'' entries are zero)
+            for (int q = 0; q < 4; ++q)
+                for (int s = 0; s < ksteps4; ++s) {
+                    const int ki = s < ksteps ? korder[s * 4 + q] : -1;
+                    coltab.push_back(static_cast<short>(cols[ki >= 0 ? ki : 0]));
+                }
+            const int npairs = (nr + 15) / 16;
+            const int noff = static_cast<int>(coltab.size());
+            for (int i = 0; i < npairs * 16; ++i) coltab.push_back(static_cast<short>(cols[i < nr ? i : 0]));
+            for (int j = 0; j < npairs; ++j) {
+                Item it{};
+                it.b_off = static_cast<int>(bf.size());
+                it.ksteps = static_cast<short>(ksteps);
+                it.ksteps4 = static_cast<short>(ksteps4);
+                it.kcol = static_cast<short>(koff);
+                it.ncol = static_cast<short>(noff + 16 * j);
+                it.nvalid = static_cast<short>(std::min(16, nr - 16 * j));
+                it.irrep = static_cast<short>(r);
+                items.push_back(it);
+                for (int s = 0; s < ksteps4; ++s)
+                    for (int f = 0; f < 2; ++f)
+                        for (int l = 0; l < 32; ++l) {
+                            const int nidx = 16 * j + 8 * f + (l >> 2);
+                            const int ki = s < ksteps ? korder[s * 4 + (l & 3)] : -1;
+                            bf.push_back(nidx < nr && ki >= 0 ? blk[static_cast<size_t>(nidx) * g.ldb + ki] : 0.0);
+                        }
+            }
+        }
+    }
+
+    // Round in which the last item of each item's irrep runs when item i runs in
+    // round i / warps; returns the largest distance to it.
+    int flush_rounds(int warps, std::vector<short> &flush) const {
+        int last[8];
+        for (int r = 0; r < 8; ++r) last[r] = -1;
+        for (size_t i = 0; i < items.size(); ++i) last[items[i].irrep] = static_cast<int>(i) / warps;
+        flush.resize(items.size());
+        int span = 0;
+        for (size_t i = 0; i < items.size(); ++i) {
+            flush[i] = static_cast<short>(last[items[i].irrep]);
+            span = std::max(span, last[items[i].irrep] - static_cast<int>(i) / warps);
+        }
+        return span;
+    }
+};
+
 }  // namespace tsvb200

@@ -72,7 +72,8 @@ class Timing(C.Structure):
 
 class SymmetryInfo(C.Structure):
     _fields_ = [("recovery_symmetric", C.c_int), ("operator_symmetric", C.c_int), ("defect_correction", C.c_int),
-                ("irrep_dofs", C.c_int * 8), ("defect_k", C.c_double * 2), ("defect_phi", C.c_double * 2)]
+                ("irrep_dofs", C.c_int * 8), ("defect_k", C.c_double * 2), ("defect_phi", C.c_double * 2),
+                ("operator_fused", C.c_int), ("reserved_", C.c_int)]
 
 
 _lib = None
