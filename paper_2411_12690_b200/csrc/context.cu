@@ -202,7 +202,6 @@ struct RomHost {
     DevBuf<int> d_fsrc, d_fdst;           // fine orbit tables (U column / Us column)
     DevBuf<GemmSeg> d_k1_segs, d_k6_segs;
     SymK1Pack k1f;                        // fused K1 (sym_k1_fused_kernel): items, column lists
-    DevBuf<double> d_kf;                  // K'' in DMMA fragment order
     // K_r - K_sym (the rounding-level symmetry defect of K_r), TF32, times 2^d_exp:
     // added back on the tensor cores so the operator stays the reference's K_r
     std::vector<float> d32_host;          // [n][n] panel order, scaled
@@ -224,7 +223,6 @@ void build_rom_symmetry(RomHost &m, const std::vector<double> &kp, const double 
     m.sym_defect_phi = pk.defect_phi;
     if (!ok) return;
     m.k1f.build(pk.red, pk.k1_segs, pk.ks, kSymKB);
-    m.d_kf.upload(m.k1f.bf.data(), m.k1f.bf.size(), stream);
     m.sred = std::move(pk.red);
     m.sfine = std::move(pk.fine);
     m.k1_segs = std::move(pk.k1_segs);
@@ -344,6 +342,8 @@ struct tsv_ctx {
         DevBuf<int4> f_tile_tab;
         DevBuf<SymK1Item> f_item_tab;
         DevBuf<short> f_col_tab;
+        DevBuf<double> f_stream[2];  // per kind: K'' fragment streams in warp order
+        int f_cpi = 0;
         // K_r symmetry-defect correction on tcgen05 (TF32): Yc32 = X32 D32^T
         bool corr = false;
         int KP = 0, NP = 0, BN = 0, ntn = 0, LD = 0, npairs = 0;
@@ -660,6 +660,7 @@ struct tsv_ctx {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, sym.f_smem));
         if (occ < 1) return false;
         sym.f_grid = std::min(sym.f_tiles, occ * sm_count);
+        if (const char *gr = std::getenv("TSV_SYM_GRID")) sym.f_grid = std::max(1, std::min(sym.f_grid, std::atoi(gr)));
         return true;
     }
 
@@ -705,6 +706,23 @@ struct tsv_ctx {
         sym.f_tiles = static_cast<int>(tiles.size());
         const bool ok = mf == 2 ? sym_fused_config<2, 8, 2>() : mf == 3 ? sym_fused_config<3, 16, 1>() : sym_fused_config<4, 16, 1>();
         if (!ok) return;
+        // K'' fragment streams: warp w reads its items (w, w + warps, ...) back to back, every
+        // item slot padded to cpi chunks of kSymKB k-steps (cpi % kSymRing == 0: the kernel's register ring)
+        int max_chunks = 1;
+        for (const auto &it : pk.items) max_chunks = std::max(max_chunks, it.ksteps4 / kSymKB);
+        sym.f_cpi = (max_chunks + kSymRing - 1) / kSymRing * kSymRing;
+        const size_t slot = static_cast<size_t>(sym.f_cpi) * kSymKB * 64;
+        for (int k = 0; k < 2; ++k) {
+            const RomHost &m = rom[k].set && rom[k].sym ? rom[k] : first;
+            std::vector<double> st(static_cast<size_t>(warps) * sym.f_rounds * slot, 0.0);
+            for (size_t i = 0; i < m.k1f.items.size() && i < pk.items.size(); ++i) {
+                const auto &it = m.k1f.items[i];
+                const size_t w = i % warps, t = i / warps;
+                std::memcpy(st.data() + (w * sym.f_rounds + t) * slot, m.k1f.bf.data() + it.b_off,
+                            static_cast<size_t>(it.ksteps4) * 64 * sizeof(double));
+            }
+            sym.f_stream[k].upload(st.data(), st.size(), stream);
+        }
         sym.f_tile_tab.upload(tiles.data(), tiles.size(), stream);
         sym.f_item_tab.upload(items.data(), items.size(), stream);
         sym.f_col_tab.upload(pk.coltab.data(), pk.coltab.size(), stream);
@@ -721,8 +739,9 @@ struct tsv_ctx {
         sp.ldk = static_cast<int>(ldk);
         sp.tiles = sym.f_tile_tab.ptr;
         sp.n_tiles = sym.f_tiles;
-        sp.Bf[0] = (rom[0].set && rom[0].sym ? rom[0] : rom[1]).d_kf.ptr;
-        sp.Bf[1] = (rom[1].set && rom[1].sym ? rom[1] : rom[0]).d_kf.ptr;
+        sp.Bf[0] = sym.f_stream[0].ptr;
+        sp.Bf[1] = sym.f_stream[1].ptr;
+        sp.cpi = sym.f_cpi;
         sp.items = sym.f_item_tab.ptr;
         sp.n_items = sym.f_items;
         sp.rounds = sym.f_rounds;
@@ -733,6 +752,7 @@ struct tsv_ctx {
         sp.done = done;
         sp.skip_flag = skip;
         sp.tile_counter = tile_counter.ptr;
+        if (const char *ab = std::getenv("TSV_SYM_ABLATE")) sp.ablate = std::atoi(ab);
         if (sym.f_mf == 2) launch_pdl(sym_k1_fused_kernel<2, 8, 2>, sym.f_grid, 256, sym.f_smem, stream, sp);
         else if (sym.f_mf == 3) launch_pdl(sym_k1_fused_kernel<3, 16, 1>, sym.f_grid, 512, sym.f_smem, stream, sp);
         else launch_pdl(sym_k1_fused_kernel<4, 16, 1>, sym.f_grid, 512, sym.f_smem, stream, sp);

@@ -16,6 +16,7 @@
 
 #include "kernels.cuh"
 #include "symmetry.hpp"
+#include "tc_local.cuh"
 
 namespace tsvb200 {
 
@@ -286,7 +287,37 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_seg_f64(GemmSegP
 // (SymK1Pack). A lane's columns for four consecutive k-steps are one 8-byte
 // load from the transposed list [lane % 4][k-step].
 constexpr int kSymSlots = 2;
-constexpr int kSymKB = 4;  // k-steps (of 4) per K'' prefetch chunk
+#ifndef TSV_SYM_KB
+#define TSV_SYM_KB 4
+#endif
+#ifndef TSV_SYM_RING
+#define TSV_SYM_RING 3
+#endif
+#ifndef TSV_SYM_VOLATILE
+#define TSV_SYM_VOLATILE 0  // 0: plain loads and DMMAs, 1: volatile K'' loads, 2: volatile loads and DMMAs
+#endif
+constexpr int kSymKB = TSV_SYM_KB;      // k-steps (of 4) per K'' chunk
+constexpr int kSymRing = TSV_SYM_RING;  // K'' chunks in the register ring (prefetch distance kSymRing - 1 chunks)
+
+// volatile: keeps the K'' prefetch loads ahead of the DMMAs they overlap (the compiler otherwise
+// sinks them behind the chunk's DMMAs to shorten live ranges, which exposes the L2 latency)
+__device__ __forceinline__ double ldg_nc_volatile(const double *p) {
+#if TSV_SYM_VOLATILE >= 1
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void dmma_8x8x4_v(double &d0, double &d1, double a, double b) {
+#if TSV_SYM_VOLATILE < 2
+    return dmma_8x8x4(d0, d1, a, b);
+#endif
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 struct SymK1Item {
     int b_off;          // first double of the item's K'' fragments [ksteps4][2][32]
@@ -306,7 +337,8 @@ struct SymK1Params {
     int ldk;                     // doubles per row copied in / out
     const int4 *tiles;           // [n_tiles] {row0, rows (<= R, multiple of 8), kind, 0}
     int n_tiles;
-    const double *Bf[2];         // per kind: K'' in fragment order
+    const double *Bf[2];         // per kind: K'' fragment streams [warp][round][cpi chunks][kSymKB][2][32]
+    int cpi;                     // chunks (of kSymKB k-steps) per item slot in the stream, a multiple of kSymRing
     const SymK1Item *items;
     int n_items, rounds;
     const short *orb;            // [n_orbits][8] plain columns of the orbit members (-1: absent)
@@ -316,6 +348,7 @@ struct SymK1Params {
     const int *done;             // nullable
     const int *skip_flag;        // nullable: early exit when != 0 (A x goes to the verification path)
     unsigned *tile_counter;
+    int ablate;                  // timing experiments only (TSV_SYM_ABLATE): 1 no K'' prefetch, 2 no butterflies, 4 no products
 };
 
 inline size_t sym_k1_smem(int mf, int ldk, int n_orbits, int n_coltab, int n_items) {
@@ -325,31 +358,45 @@ inline size_t sym_k1_smem(int mf, int ldk, int n_orbits, int n_coltab, int n_ite
     return (b + 15) / 16 * 16;
 }
 
-// In-place butterflies over every (row, orbit) of the tile; INV: 1 / |orbit|.
-template <bool INV, int THREADS>
+// In-place butterflies over every (row, orbit) of the tile (a warp per row,
+// lanes over orbits); INV: 1 / |orbit|.
+template <bool INV, int WARPS>
 __device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int R, const short *orb, int n_orbits) {
-    for (int t = threadIdx.x; t < R * n_orbits; t += THREADS) {
-        const int r = t / n_orbits, o = t - r * n_orbits;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = lane; o < n_orbits; o += 32) {
         const int4 mv = *reinterpret_cast<const int4 *>(orb + o * 8);
         short m[8];
         m[0] = static_cast<short>(mv.x), m[1] = static_cast<short>(mv.x >> 16);
         m[2] = static_cast<short>(mv.y), m[3] = static_cast<short>(mv.y >> 16);
         m[4] = static_cast<short>(mv.z), m[5] = static_cast<short>(mv.z >> 16);
         m[6] = static_cast<short>(mv.w), m[7] = static_cast<short>(mv.w >> 16);
-        double *row = xs + r * P;
-        double x[8];
         int f = 0;
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            x[g] = m[g] >= 0 ? row[m[g]] : 0.0;
-            if (m[g] >= 0) f |= g;
-        }
-        sym_butterfly(x, f);
-        const double s = !INV ? 1.0 : f == 7 ? 0.125 : (f == 0 ? 1.0 : ((f & (f - 1)) == 0 ? 0.5 : 0.25));
-#pragma unroll
         for (int g = 0; g < 8; ++g)
-            if (m[g] >= 0) row[m[g]] = INV ? s * x[g] : x[g];
+            if (m[g] >= 0) f |= g;
+        const double s = !INV ? 1.0 : f == 7 ? 0.125 : (f == 0 ? 1.0 : ((f & (f - 1)) == 0 ? 0.5 : 0.25));
+#pragma unroll 2
+        for (int r = warp; r < R; r += WARPS) {
+            double *row = xs + r * P;
+            double x[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) x[g] = m[g] >= 0 ? row[m[g]] : 0.0;
+            sym_butterfly(x, f);
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                if (m[g] >= 0) row[m[g]] = INV ? s * x[g] : x[g];
+        }
     }
+}
+
+// 1-D bulk copies (TMA unit) of whole panel rows
+__device__ __forceinline__ void bulk_load_row(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store_row(void *dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes) : "memory");
 }
 
 template <int MF, int WARPS, int MINB>
@@ -372,38 +419,50 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
         for (int i = tid; i < p.n_orbits * 8; i += THREADS) orb[i] = p.orb[i];
         for (int i = tid; i < p.n_coltab; i += THREADS) coltab[i] = p.coltab[i];
     }
-    const int cpr = p.ldk / 2;  // 16-byte chunks per row
+    __shared__ __align__(8) uint64_t row_bar;
+    const uint32_t bar = smem_u32(&row_bar);
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const uint32_t row_bytes = static_cast<uint32_t>(p.ldk) * 8u;
+    uint32_t phase = 0;
     while (!skip) {
-        if (tid == 0) s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
+        if (tid == 0) {
+            s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
+            // the previous tile's rows have left shared memory before it is overwritten
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncthreads();
         const int tile = s_tile;
         if (tile >= p.n_tiles) break;
         const int4 tl = p.tiles[tile];
         const int rows = tl.y;
         const double *Bf = tl.z ? p.Bf[1] : p.Bf[0];
-        // ---- rows in (absent rows of a short tile: zeros)
-        {
+        // ---- rows in: one bulk copy per row (absent rows of a short tile: zeros)
+        if (tid == 0) {
+            mbar_expect_tx(bar, row_bytes * static_cast<uint32_t>(rows));
             const double *src = p.X + static_cast<long long>(tl.x) * p.ld;
-            for (int i = tid; i < R * cpr; i += THREADS) {
-                const int r = i / cpr, c = i - r * cpr;
-                if (r < rows) cp_async16(xs + r * P + 2 * c, src + r * p.ld + 2 * c);
-                else *reinterpret_cast<double2 *>(xs + r * P + 2 * c) = make_double2(0.0, 0.0);
-            }
-            cp_async_commit();
+            for (int r = 0; r < rows; ++r) bulk_load_row(smem_u32(xs + r * P), src + r * p.ld, row_bytes, bar);
         }
-        // the first K'' chunk of this warp's first item while the rows land
-        double bc[kSymKB][2], bn[kSymKB][2];
-        if (warp < p.n_items) {
-            const double *bp = Bf + items[warp].b_off + lane;
+        for (int i = tid; i < (R - rows) * p.ldk; i += THREADS) xs[rows * P + (i / p.ldk) * P + i % p.ldk] = 0.0;
+        // K'' register ring: the warp's fragment stream is contiguous over its items,
+        // chunk g of the stream lives in b[g % kSymRing] (cpi % kSymRing == 0)
+        double b[kSymRing][kSymKB][2];
+        const double *bw = Bf + static_cast<long long>(warp) * p.rounds * p.cpi * (kSymKB * 64) + lane;
+        const int stream_chunks = p.rounds * p.cpi;
+#pragma unroll
+        for (int u = 0; u < kSymRing - 1; ++u)
 #pragma unroll
             for (int s = 0; s < kSymKB; ++s) {
-                bc[s][0] = __ldg(bp + (2 * s) * 32);
-                bc[s][1] = __ldg(bp + (2 * s + 1) * 32);
+                b[u][s][0] = ldg_nc_volatile(bw + (u * kSymKB + s) * 64);
+                b[u][s][1] = ldg_nc_volatile(bw + (u * kSymKB + s) * 64 + 32);
             }
-        }
-        cp_async_wait<0>();
+        mbar_wait(bar, phase);
+        phase ^= 1u;
         __syncthreads();
-        sym_tile_butterflies<false, THREADS>(xs, P, R, orb, p.n_orbits);
+        if (!(p.ablate & 2)) sym_tile_butterflies<false, WARPS>(xs, P, R, orb, p.n_orbits);
         __syncthreads();
         // ---- irrep products
         double acc[kSymSlots][MF][2][2];
@@ -416,42 +475,49 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
             for (int v = 0; v < kSymSlots; ++v) {
                 const int t = t0 + v;
                 const int it = t * WARPS + warp;
-                if (t < p.rounds && it < p.n_items) {
+                if (t < p.rounds && it < p.n_items && !(p.ablate & 4)) {
                     const SymK1Item item = items[it];
 #pragma unroll
                     for (int i = 0; i < MF; ++i) acc[v][i][0][0] = acc[v][i][0][1] = acc[v][i][1][0] = acc[v][i][1][1] = 0.0;
-                    const double *bp = Bf + item.b_off + lane;
                     const short *kc = coltab + item.kcol + (lane & 3) * item.ksteps4;
                     const int ks = item.ksteps;
-                    const bool more = it + WARPS < p.n_items;
-                    const double *bp_next = more ? Bf + items[it + WARPS].b_off + lane : bp;
-                    for (int s0 = 0; s0 < ks; s0 += kSymKB) {
-                        const bool last = s0 + kSymKB >= ks;
-                        if (!last || more) {
-                            const double *q = last ? bp_next : bp + (s0 + kSymKB) * 64;
+                    for (int c0 = 0; c0 < p.cpi; c0 += kSymRing) {
 #pragma unroll
-                            for (int s = 0; s < kSymKB; ++s) {
-                                bn[s][0] = __ldg(q + (2 * s) * 32);
-                                bn[s][1] = __ldg(q + (2 * s + 1) * 32);
-                            }
-                        }
-                        const short4 cv = *reinterpret_cast<const short4 *>(kc + s0);
-                        const int cols[4] = {cv.x, cv.y, cv.z, cv.w};
+                        for (int u = 0; u < kSymRing; ++u) {
+                            const int c = c0 + u, s0 = c * kSymKB, g = t * p.cpi + c;
+                            constexpr int kAhead = kSymRing - 1;
+                            if (g + kAhead < stream_chunks && !(p.ablate & 1)) {
+                                const double *q = bw + static_cast<long long>(g + kAhead) * (kSymKB * 64);
 #pragma unroll
-                        for (int s = 0; s < kSymKB; ++s) {
-                            if (s < 2 || s0 + s < ks) {  // ksteps is even: only the second half of a chunk can be absent
-                                double af[MF];
-#pragma unroll
-                                for (int i = 0; i < MF; ++i) af[i] = arow[i * 8 * P + cols[s]];
-#pragma unroll
-                                for (int i = 0; i < MF; ++i) {
-                                    dmma_8x8x4(acc[v][i][0][0], acc[v][i][0][1], af[i], bc[s][0]);
-                                    dmma_8x8x4(acc[v][i][1][0], acc[v][i][1][1], af[i], bc[s][1]);
+                                for (int s = 0; s < kSymKB; ++s) {
+                                    b[(u + kAhead) % kSymRing][s][0] = ldg_nc_volatile(q + s * 64);
+                                    b[(u + kAhead) % kSymRing][s][1] = ldg_nc_volatile(q + s * 64 + 32);
                                 }
                             }
-                        }
+                            if (s0 < ks) {  // ksteps is even: whole chunks (padding k-steps inside ksteps read a real column; their K'' is zero)
+                                int cols[kSymKB];
+                                if constexpr (kSymKB == 2) {
+                                    const short2 cv = *reinterpret_cast<const short2 *>(kc + s0);
+                                    cols[0] = cv.x, cols[1] = cv.y;
+                                } else {
+                                    static_assert(kSymKB == 2 || kSymKB == 4, "kSymKB");
+                                    const short4 cv = *reinterpret_cast<const short4 *>(kc + s0);
+                                    cols[0] = cv.x, cols[1] = cv.y, cols[2] = cv.z, cols[3] = cv.w;
+                                }
+                                double af[kSymKB][MF];
 #pragma unroll
-                        for (int s = 0; s < kSymKB; ++s) bc[s][0] = bn[s][0], bc[s][1] = bn[s][1];
+                                for (int s = 0; s < kSymKB; ++s)
+#pragma unroll
+                                    for (int i = 0; i < MF; ++i) af[s][i] = arow[i * 8 * P + cols[s]];
+#pragma unroll
+                                for (int s = 0; s < kSymKB; ++s)
+#pragma unroll
+                                    for (int i = 0; i < MF; ++i) {
+                                        dmma_8x8x4_v(acc[v][i][0][0], acc[v][i][0][1], af[s][i], b[u][s][0]);
+                                        dmma_8x8x4_v(acc[v][i][1][0], acc[v][i][1][1], af[s][i], b[u][s][1]);
+                                    }
+                            }
+                        }
                     }
                     pend_round[v] = item.flush_round;
                     pend_ncol[v] = item.ncol;
@@ -482,18 +548,17 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
             }
         }
         __syncthreads();
-        sym_tile_butterflies<true, THREADS>(xs, P, R, orb, p.n_orbits);
+        if (!(p.ablate & 2)) sym_tile_butterflies<true, WARPS>(xs, P, R, orb, p.n_orbits);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes before the bulk stores
         __syncthreads();
         // ---- rows out
-        {
+        if (tid == 0) {
             double *dst = p.Y + static_cast<long long>(tl.x) * p.ld;
-            for (int i = tid; i < rows * cpr; i += THREADS) {
-                const int r = i / cpr, c = i - r * cpr;
-                *reinterpret_cast<double2 *>(dst + r * p.ld + 2 * c) = *reinterpret_cast<const double2 *>(xs + r * P + 2 * c);
-            }
+            for (int r = 0; r < rows; ++r) bulk_store_row(dst + r * p.ld, smem_u32(xs + r * P), row_bytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        __syncthreads();
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     pdl_trigger();
     if (tid == 0) {
         __threadfence();

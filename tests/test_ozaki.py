@@ -52,13 +52,15 @@ def test_int8_operator_solve_matches_reference(oracle_libs, native_lib, monkeypa
         assert rel_l2(sol.u, u_r) <= 1e-10
 
 
-def test_hybrid_verification_is_default_for_schwarz(oracle_libs, native_lib, monkeypatch):
-    """Schwarz PCG: A p on DMMA, the true-residual A x on int8 (TSV_K1_VERIFY
-    default 10); with the hybrid off the answer is the same within the bar."""
+def test_hybrid_verification_matches_fp64_check(oracle_libs, native_lib, monkeypatch):
+    """Schwarz PCG with the A x of the true-residual check on int8
+    (TSV_K1_VERIFY=10: the default when the irrep K1 carries the iteration,
+    opt-in on the plain DMMA path) against the FP64 DMMA check: the same
+    answer within the bar, two more (early-exit) launches per iteration."""
     refpy, _ = oracle_libs
     sess, g = _case(refpy, True)
     u_r, _, _ = sess.iterate(1e-12)
-    monkeypatch.delenv("TSV_K1_VERIFY", raising=False)
+    monkeypatch.setenv("TSV_K1_VERIFY", "10")
     a = g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
     monkeypatch.setenv("TSV_K1_VERIFY", "0")
     b = g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
