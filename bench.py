@@ -305,8 +305,17 @@ def run_ours(args, cfg, rank, local_rank, world):
 
     # dominant kernel (K1 operator apply) on its own stream, CUDA events
     k1_ms = g.profile_apply(50)
-    k1_flops = 2.0 * cfg.n ** 2 * cfg.B
     dmma_peak = ctypes_peak(L, dev)
+    # Mirror-symmetric ROMs: K1 / K6 run as 8 irrep products (sum n_r^2 instead of
+    # n^2 multiply-adds per block). `k1_flops` is the work the kernel executes;
+    # the dense figure 2 n^2 B of north_star's contraction is reported beside it.
+    sym = g.symmetry()
+    k1_dense_flops = 2.0 * cfg.n ** 2 * cfg.B
+    irrep = [d for d in sym["irrep_dofs"] if d] if sym["operator"] else []
+    k1_flops = 2.0 * sum(d * d for d in irrep) * cfg.B if irrep else k1_dense_flops
+    k6_dense_flops = 2.0 * cfg.n_fine * cfg.n * cfg.B
+    # irrep K6: the dense basis rows split over the irreps like the reduced DoFs (1/8 to rounding)
+    k6_flops = k6_dense_flops * (k1_flops / k1_dense_flops) if sym["recovery"] else k6_dense_flops
 
     # the same step with the reference's own Jacobi-PCG (one timed step): the
     # per-iteration kernel path the reference's preconditioner implies
@@ -350,7 +359,8 @@ def run_ours(args, cfg, rank, local_rank, world):
     nc = pinfo["coarse_dofs"]
     # FP64 contractions only (K1 per iteration + K6 once): the TF32 local solves
     # of the Schwarz preconditioner are HBM-bound and charged as bytes below
-    flops_step = iters * 2.0 * cfg.n ** 2 * cfg.B + 2.0 * cfg.n_fine * cfg.n * cfg.B
+    flops_step = iters * k1_flops + k6_flops
+    flops_step_dense = iters * k1_dense_flops + k6_dense_flops
     out_bytes = cfg.B * cfg.elements * cfg.points * 7 * 8
     hbm_peak = measured_hbm()
     if schwarz:
@@ -360,8 +370,14 @@ def run_ours(args, cfg, rank, local_rank, world):
         vec_bytes = 136.0 * ix.dof_count + 16.0 * cfg.n * cfg.B + 2.0 * nc * nc
     else:
         vec_bytes = 104.0 * ix.dof_count
-    t_roof_ms = 1e3 * (iters * (2.0 * cfg.n ** 2 * cfg.B / (dmma_peak * 1e12) + vec_bytes / (hbm_peak * 1e9))
-                       + max(2.0 * cfg.n_fine * cfg.n * cfg.B / (dmma_peak * 1e12), out_bytes / (hbm_peak * 1e9)))
+    # Executed-work model: K1 at the DMMA peak on the FLOPs it executes (or its X-in / Y-out panel
+    # stream, whichever is longer), the vector / panel / coarse bytes at the HBM peak, recovery as K6
+    # beside the stress stream. The dense model charges north_star's 2 n^2 B and 2 n_fine n B instead.
+    panel_bytes = 16.0 * cfg.n * cfg.B
+    t_roof_ms = 1e3 * (iters * (max(k1_flops / (dmma_peak * 1e12), panel_bytes / (hbm_peak * 1e9)) + vec_bytes / (hbm_peak * 1e9))
+                       + max(k6_flops / (dmma_peak * 1e12), out_bytes / (hbm_peak * 1e9)))
+    t_roof_dense_ms = 1e3 * (iters * (k1_dense_flops / (dmma_peak * 1e12) + vec_bytes / (hbm_peak * 1e9))
+                             + max(k6_dense_flops / (dmma_peak * 1e12), out_bytes / (hbm_peak * 1e9)))
     line = {
         "metric": METRIC, "value": value, "unit": "blocks/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -373,17 +389,29 @@ def run_ours(args, cfg, rank, local_rank, world):
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2: {out_bytes / 1e9:.1f} GB stress output + {ix.dof_count * 8 * 6 / 1e6:.0f} MB vectors per step"},
         "roofline": {"bound": "tensor", "achieved": k1_flops / (k1_ms * 1e-3) / 1e12, "peak": dmma_peak,
-                     "unit": "TFLOP/s", "frac": k1_flops / (k1_ms * 1e-3) / 1e12 / dmma_peak, "traffic": k1_traffic(cfg),
-                     "kernel": "gemm_nt_f64 (K1 operator apply, 2n^2 B FLOP per launch)",
+                     "unit": "TFLOP/s", "frac": k1_flops / (k1_ms * 1e-3) / 1e12 / dmma_peak,
+                     "traffic": k1_traffic(cfg, bool(irrep)),
+                     "kernel": ("sym_k1_fused_kernel (K1 operator apply on the 8 irrep blocks of a mirror-symmetric K_r: "
+                                "2 sum n_r^2 B FLOP per launch)" if irrep else
+                                "gemm_nt_f64 (K1 operator apply, 2n^2 B FLOP per launch)"),
+                     "irrep_dofs": irrep or None,
+                     "dense_equivalent": {"tflops": k1_dense_flops / (k1_ms * 1e-3) / 1e12,
+                                          "frac": k1_dense_flops / (k1_ms * 1e-3) / 1e12 / dmma_peak,
+                                          "what": "the same launch charged with north_star's dense 2 n^2 B FLOP"},
                      "peak_source": "measured live: register-only DMMA.8x8x4 loop (tsv_fp64_peak); MEASURED_PEAKS.json has no FP64 entry"},
         "end_to_end_roofline": {"t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms_step,
-                                "model": ("iters*(2n^2B/P64 + (136N + 16nB + 2Nc^2)/BW) + max(2 n_fine n B/P64, 56 B/point/BW)"
-                                          if schwarz else "iters*(2n^2B/P64 + 104N/BW) + max(2 n_fine n B/P64, 56 B/point/BW)"),
+                                "model": ("iters*(max(K1 FLOP/P64, 16nB/BW) + (136N + 16nB + 2Nc^2)/BW) + max(K6 FLOP/P64, 56 B/point/BW)"
+                                          if schwarz else "iters*(max(K1 FLOP/P64, 16nB/BW) + 104N/BW) + max(K6 FLOP/P64, 56 B/point/BW)"),
+                                "flop_model": "executed (irrep blocks)" if irrep else "dense",
+                                "dense_model": {"t_roof_ms": t_roof_dense_ms, "frac": t_roof_dense_ms / ms_step,
+                                                "what": "K1 = 2 n^2 B and K6 = 2 n_fine n B FLOP at the DMMA peak (round-1/2 model)"},
                                 "hbm_gbs": hbm_peak},
         "value_with_setup": {"value": aggregate_throughput(cfg.B, world, ms_step + pinfo["setup_ms_warm"]),
                              "ms_per_step": ms_step + pinfo["setup_ms_warm"],
                              "what": "one solve + recovery per layout: the warm preconditioner set-up added to the step"},
         "gflops": flops_step / (ms_step * 1e-3) / 1e9,
+        "gflops_dense_equivalent": flops_step_dense / (ms_step * 1e-3) / 1e9,
+        "symmetry": {k: sym[k] for k in ("recovery", "operator", "fused", "defect_k", "defect_phi")},
         "phase_ms": {"solve": solve_ms, "recover": recover_ms, "k1_per_launch": k1_ms,
                      "per_iteration": solve_ms / max(1, iters)},
         "rom_build_s": t_rom,
@@ -402,10 +430,10 @@ def run_ours(args, cfg, rank, local_rank, world):
     return 0
 
 
-def k1_traffic(cfg):
+def k1_traffic(cfg, irrep=False):
     """DRAM bytes per K1 launch from the committed ncu capture (profiles/k1_traffic.json), or None."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))[cfg.name]
+        t = json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))[cfg.name + ("/irrep" if irrep else "")]
         return t["dram_read_bytes"] + t["dram_write_bytes"]
     except (OSError, KeyError, ValueError):
         return None

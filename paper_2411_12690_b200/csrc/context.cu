@@ -706,6 +706,21 @@ struct tsv_ctx {
         sym.f_tiles = static_cast<int>(tiles.size());
         const bool ok = mf == 2 ? sym_fused_config<2, 8, 2>() : mf == 3 ? sym_fused_config<3, 16, 1>() : sym_fused_config<4, 16, 1>();
         if (!ok) return;
+        // Balanced tail: the tiles past the last full wave of the grid are cut into single row
+        // fragments (8 rows: half the butterflies and products of a 16-row tile), so the last
+        // wave is short instead of leaving most CTAs idle for a whole tile
+        {
+            const int T = static_cast<int>(tiles.size()), rem = T > sym.f_grid ? T % sym.f_grid : 0;
+            const char *bt = std::getenv("TSV_SYM_K1_TAIL");
+            if (rem > 0 && rem * mf <= sym.f_grid && !(bt && *bt == '0')) {
+                std::vector<int4> cut(tiles.begin(), tiles.end() - rem);
+                for (int i = T - rem; i < T; ++i)
+                    for (int r = 0; r < tiles[i].y; r += 8)
+                        cut.push_back(make_int4(tiles[i].x + r, std::min(8, tiles[i].y - r), tiles[i].z, 0));
+                tiles.swap(cut);
+                sym.f_tiles = static_cast<int>(tiles.size());
+            }
+        }
         // K'' fragment streams: warp w reads its items (w, w + warps, ...) back to back, every
         // item slot padded to cpi chunks of kSymKB k-steps (cpi % kSymRing == 0: the kernel's register ring)
         int max_chunks = 1;

@@ -354,37 +354,49 @@ struct SymK1Params {
 inline size_t sym_k1_smem(int mf, int ldk, int n_orbits, int n_coltab, int n_items) {
     size_t b = static_cast<size_t>(mf) * 8 * (ldk + 4) * sizeof(double);
     b += static_cast<size_t>(n_items) * sizeof(SymK1Item);
-    b += (static_cast<size_t>(n_orbits) * 8 + n_coltab) * sizeof(short);
+    b += (static_cast<size_t>(n_orbits) * 16 + n_coltab) * sizeof(short);
     return (b + 15) / 16 * 16;
 }
 
-// In-place butterflies over every (row, orbit) of the tile (a warp per row,
-// lanes over orbits); INV: 1 / |orbit|.
+// In-place butterflies over every (row, orbit) of the tile. A half-warp takes
+// 4 consecutive orbits x 4 rows (lane = 4 row + orbit), so with the row pitch
+// = 4 mod 16 doubles an 8-byte access to member g of the four orbits is
+// conflict-free when their columns differ mod 4 - the orbit order of the host
+// tables (SymTables::order_orbits_for_banks). orbL / orbS: the members' columns
+// for the loads / stores [n_orbits][8]; an absent member loads the row's zero
+// column and stores to its sink column, so the three butterfly stages run
+// unconditionally (a stage over an axis the orbit does not move adds zeros to
+// the present members and only touches absent ones otherwise). INV: scaled by
+// 1 / |orbit|.
 template <bool INV, int WARPS>
-__device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int R, const short *orb, int n_orbits) {
+__device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int rows, const short *orbL, const short *orbS,
+                                                     int n_orbits, int zcol) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int o = lane; o < n_orbits; o += 32) {
-        const int4 mv = *reinterpret_cast<const int4 *>(orb + o * 8);
-        short m[8];
-        m[0] = static_cast<short>(mv.x), m[1] = static_cast<short>(mv.x >> 16);
-        m[2] = static_cast<short>(mv.y), m[3] = static_cast<short>(mv.y >> 16);
-        m[4] = static_cast<short>(mv.z), m[5] = static_cast<short>(mv.z >> 16);
-        m[6] = static_cast<short>(mv.w), m[7] = static_cast<short>(mv.w >> 16);
-        int f = 0;
+    const int r0 = lane >> 2;  // 0..7: row within a block of 8
+    for (int o = warp * 4 + (lane & 3); o < n_orbits; o += WARPS * 4) {
+        const int4 lv = *reinterpret_cast<const int4 *>(orbL + o * 8);
+        const int4 sv = *reinterpret_cast<const int4 *>(orbS + o * 8);
+        int ml[8], ms[8];
+        ml[0] = lv.x & 0xffff, ml[1] = static_cast<unsigned>(lv.x) >> 16, ml[2] = lv.y & 0xffff, ml[3] = static_cast<unsigned>(lv.y) >> 16;
+        ml[4] = lv.z & 0xffff, ml[5] = static_cast<unsigned>(lv.z) >> 16, ml[6] = lv.w & 0xffff, ml[7] = static_cast<unsigned>(lv.w) >> 16;
+        ms[0] = sv.x & 0xffff, ms[1] = static_cast<unsigned>(sv.x) >> 16, ms[2] = sv.y & 0xffff, ms[3] = static_cast<unsigned>(sv.y) >> 16;
+        ms[4] = sv.z & 0xffff, ms[5] = static_cast<unsigned>(sv.z) >> 16, ms[6] = sv.w & 0xffff, ms[7] = static_cast<unsigned>(sv.w) >> 16;
+        double s = 1.0;
+        if (INV) {
+            int members = 0;
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if (m[g] >= 0) f |= g;
-        const double s = !INV ? 1.0 : f == 7 ? 0.125 : (f == 0 ? 1.0 : ((f & (f - 1)) == 0 ? 0.5 : 0.25));
+            for (int g = 0; g < 8; ++g) members += ml[g] != zcol;
+            s = 1.0 / static_cast<double>(members);  // 1, 2, 4 or 8 members: exact
+        }
 #pragma unroll 2
-        for (int r = warp; r < R; r += WARPS) {
+        for (int r = r0; r < rows; r += 8) {
             double *row = xs + r * P;
             double x[8];
 #pragma unroll
-            for (int g = 0; g < 8; ++g) x[g] = m[g] >= 0 ? row[m[g]] : 0.0;
-            sym_butterfly(x, f);
+            for (int g = 0; g < 8; ++g) x[g] = row[ml[g]];
+            sym_butterfly(x, 7);
 #pragma unroll
-            for (int g = 0; g < 8; ++g)
-                if (m[g] >= 0) row[m[g]] = INV ? s * x[g] : x[g];
+            for (int g = 0; g < 8; ++g) row[ms[g]] = INV ? s * x[g] : x[g];
         }
     }
 }
@@ -399,6 +411,96 @@ __device__ __forceinline__ void bulk_store_row(void *dst, uint32_t src, uint32_t
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes) : "memory");
 }
 
+// The irrep products of one tile on MF row fragments (the kernel's inner part).
+template <int MF, int WARPS>
+__device__ __forceinline__ void sym_tile_products(const SymK1Params &p, double *xs, int P, const SymK1Item *items,
+                                                  const short *coltab, double (&b)[kSymRing][kSymKB][2], const double *bw,
+                                                  int stream_chunks) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc[kSymSlots][MF][2][2];
+    int pend_round[kSymSlots], pend_ncol[kSymSlots], pend_nvalid[kSymSlots];
+#pragma unroll
+    for (int v = 0; v < kSymSlots; ++v) pend_round[v] = -1;
+    const double *arow = xs + (lane >> 2) * P;
+    for (int t0 = 0; t0 < p.rounds; t0 += kSymSlots) {
+#pragma unroll
+        for (int v = 0; v < kSymSlots; ++v) {
+            const int t = t0 + v;
+            const int it = t * WARPS + warp;
+            if (t < p.rounds && it < p.n_items && !(p.ablate & 4)) {
+                const SymK1Item item = items[it];
+#pragma unroll
+                for (int i = 0; i < MF; ++i) acc[v][i][0][0] = acc[v][i][0][1] = acc[v][i][1][0] = acc[v][i][1][1] = 0.0;
+                const short *kc = coltab + item.kcol + (lane & 3) * item.ksteps4;
+                const int ks = item.ksteps;
+                for (int c0 = 0; c0 < p.cpi; c0 += kSymRing) {
+#pragma unroll
+                    for (int u = 0; u < kSymRing; ++u) {
+                        const int c = c0 + u, s0 = c * kSymKB, g = t * p.cpi + c;
+                        constexpr int kAhead = kSymRing - 1;
+                        if (g + kAhead < stream_chunks && !(p.ablate & 1)) {
+                            const double *q = bw + static_cast<long long>(g + kAhead) * (kSymKB * 64);
+#pragma unroll
+                            for (int s = 0; s < kSymKB; ++s) {
+                                b[(u + kAhead) % kSymRing][s][0] = ldg_nc_volatile(q + s * 64);
+                                b[(u + kAhead) % kSymRing][s][1] = ldg_nc_volatile(q + s * 64 + 32);
+                            }
+                        }
+                        if (s0 < ks) {  // ksteps is even: whole chunks (padding k-steps inside ksteps read a real column; their K'' is zero)
+                            int cols[kSymKB];
+                            if constexpr (kSymKB == 2) {
+                                const short2 cv = *reinterpret_cast<const short2 *>(kc + s0);
+                                cols[0] = cv.x, cols[1] = cv.y;
+                            } else {
+                                static_assert(kSymKB == 2 || kSymKB == 4, "kSymKB");
+                                const short4 cv = *reinterpret_cast<const short4 *>(kc + s0);
+                                cols[0] = cv.x, cols[1] = cv.y, cols[2] = cv.z, cols[3] = cv.w;
+                            }
+                            double af[kSymKB][MF];
+#pragma unroll
+                            for (int s = 0; s < kSymKB; ++s)
+#pragma unroll
+                                for (int i = 0; i < MF; ++i) af[s][i] = arow[i * 8 * P + cols[s]];
+#pragma unroll
+                            for (int s = 0; s < kSymKB; ++s)
+#pragma unroll
+                                for (int i = 0; i < MF; ++i) {
+                                    dmma_8x8x4_v(acc[v][i][0][0], acc[v][i][0][1], af[s][i], b[u][s][0]);
+                                    dmma_8x8x4_v(acc[v][i][1][0], acc[v][i][1][1], af[s][i], b[u][s][1]);
+                                }
+                        }
+                    }
+                }
+                pend_round[v] = item.flush_round;
+                pend_ncol[v] = item.ncol;
+                pend_nvalid[v] = item.nvalid;
+            }
+            __syncthreads();  // round t done: operands of irreps that ended in it are dead
+            if (t < p.rounds) {
+#pragma unroll
+                for (int w = 0; w < kSymSlots; ++w) {
+                    if (pend_round[w] >= 0 && pend_round[w] <= t) {
+                        double *orow = xs + (lane >> 2) * P;
+#pragma unroll
+                        for (int fr = 0; fr < 2; ++fr) {
+                            const int j = 8 * fr + 2 * (lane & 3);
+                            const short *nc = coltab + pend_ncol[w] + j;
+                            const int c0 = nc[0], c1 = nc[1];
+                            const bool v0 = j < pend_nvalid[w], v1 = j + 1 < pend_nvalid[w];
+#pragma unroll
+                            for (int i = 0; i < MF; ++i) {
+                                if (v0) orow[i * 8 * P + c0] = acc[w][i][fr][0];
+                                if (v1) orow[i * 8 * P + c1] = acc[w][i][fr][1];
+                            }
+                        }
+                        pend_round[w] = -1;
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int MF, int WARPS, int MINB>
 __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Params p) {
     pdl_wait();
@@ -408,15 +510,22 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
     const int P = p.ldk + 4;
     double *xs = sym_smem;
     SymK1Item *items = reinterpret_cast<SymK1Item *>(xs + static_cast<size_t>(R) * P);
-    short *orb = reinterpret_cast<short *>(items + p.n_items);
-    short *coltab = orb + p.n_orbits * 8;
+    short *orbL = reinterpret_cast<short *>(items + p.n_items);  // load / store columns of the orbit members
+    short *orbS = orbL + p.n_orbits * 8;
+    short *coltab = orbS + p.n_orbits * 8;
+    const int zcol = p.ldk, sink = p.ldk + 2;  // in the row pitch padding: always zero / write-only
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool skip = (p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) ||
                       (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0);
     if (!skip) {
         for (int i = tid; i < p.n_items * 4; i += THREADS)
             reinterpret_cast<int *>(items)[i] = reinterpret_cast<const int *>(p.items)[i];
-        for (int i = tid; i < p.n_orbits * 8; i += THREADS) orb[i] = p.orb[i];
+        for (int i = tid; i < p.n_orbits * 8; i += THREADS) {
+            const short c = p.orb[i];
+            orbL[i] = c >= 0 ? c : static_cast<short>(zcol);
+            orbS[i] = c >= 0 ? c : static_cast<short>(sink);
+        }
+        for (int r = tid; r < R; r += THREADS) xs[r * P + zcol] = 0.0;
         for (int i = tid; i < p.n_coltab; i += THREADS) coltab[i] = p.coltab[i];
     }
     __shared__ __align__(8) uint64_t row_bar;
@@ -446,7 +555,10 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
             const double *src = p.X + static_cast<long long>(tl.x) * p.ld;
             for (int r = 0; r < rows; ++r) bulk_load_row(smem_u32(xs + r * P), src + r * p.ld, row_bytes, bar);
         }
-        for (int i = tid; i < (R - rows) * p.ldk; i += THREADS) xs[rows * P + (i / p.ldk) * P + i % p.ldk] = 0.0;
+        {   // rows of the last active fragment beyond the tile (tiles are whole fragments unless a kind group is not): zeros
+            const int rpad = (rows + 7) / 8 * 8;
+            for (int i = tid; i < (rpad - rows) * p.ldk; i += THREADS) xs[rows * P + (i / p.ldk) * P + i % p.ldk] = 0.0;
+        }
         // K'' register ring: the warp's fragment stream is contiguous over its items,
         // chunk g of the stream lives in b[g % kSymRing] (cpi % kSymRing == 0)
         double b[kSymRing][kSymKB][2];
@@ -462,93 +574,21 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
         mbar_wait(bar, phase);
         phase ^= 1u;
         __syncthreads();
-        if (!(p.ablate & 2)) sym_tile_butterflies<false, WARPS>(xs, P, R, orb, p.n_orbits);
+        if (!(p.ablate & 2)) sym_tile_butterflies<false, WARPS>(xs, P, rows, orbL, orbS, p.n_orbits, zcol);
         __syncthreads();
-        // ---- irrep products
-        double acc[kSymSlots][MF][2][2];
-        int pend_round[kSymSlots], pend_ncol[kSymSlots], pend_nvalid[kSymSlots];
-#pragma unroll
-        for (int v = 0; v < kSymSlots; ++v) pend_round[v] = -1;
-        const double *arow = xs + (lane >> 2) * P;
-        for (int t0 = 0; t0 < p.rounds; t0 += kSymSlots) {
-#pragma unroll
-            for (int v = 0; v < kSymSlots; ++v) {
-                const int t = t0 + v;
-                const int it = t * WARPS + warp;
-                if (t < p.rounds && it < p.n_items && !(p.ablate & 4)) {
-                    const SymK1Item item = items[it];
-#pragma unroll
-                    for (int i = 0; i < MF; ++i) acc[v][i][0][0] = acc[v][i][0][1] = acc[v][i][1][0] = acc[v][i][1][1] = 0.0;
-                    const short *kc = coltab + item.kcol + (lane & 3) * item.ksteps4;
-                    const int ks = item.ksteps;
-                    for (int c0 = 0; c0 < p.cpi; c0 += kSymRing) {
-#pragma unroll
-                        for (int u = 0; u < kSymRing; ++u) {
-                            const int c = c0 + u, s0 = c * kSymKB, g = t * p.cpi + c;
-                            constexpr int kAhead = kSymRing - 1;
-                            if (g + kAhead < stream_chunks && !(p.ablate & 1)) {
-                                const double *q = bw + static_cast<long long>(g + kAhead) * (kSymKB * 64);
-#pragma unroll
-                                for (int s = 0; s < kSymKB; ++s) {
-                                    b[(u + kAhead) % kSymRing][s][0] = ldg_nc_volatile(q + s * 64);
-                                    b[(u + kAhead) % kSymRing][s][1] = ldg_nc_volatile(q + s * 64 + 32);
-                                }
-                            }
-                            if (s0 < ks) {  // ksteps is even: whole chunks (padding k-steps inside ksteps read a real column; their K'' is zero)
-                                int cols[kSymKB];
-                                if constexpr (kSymKB == 2) {
-                                    const short2 cv = *reinterpret_cast<const short2 *>(kc + s0);
-                                    cols[0] = cv.x, cols[1] = cv.y;
-                                } else {
-                                    static_assert(kSymKB == 2 || kSymKB == 4, "kSymKB");
-                                    const short4 cv = *reinterpret_cast<const short4 *>(kc + s0);
-                                    cols[0] = cv.x, cols[1] = cv.y, cols[2] = cv.z, cols[3] = cv.w;
-                                }
-                                double af[kSymKB][MF];
-#pragma unroll
-                                for (int s = 0; s < kSymKB; ++s)
-#pragma unroll
-                                    for (int i = 0; i < MF; ++i) af[s][i] = arow[i * 8 * P + cols[s]];
-#pragma unroll
-                                for (int s = 0; s < kSymKB; ++s)
-#pragma unroll
-                                    for (int i = 0; i < MF; ++i) {
-                                        dmma_8x8x4_v(acc[v][i][0][0], acc[v][i][0][1], af[s][i], b[u][s][0]);
-                                        dmma_8x8x4_v(acc[v][i][1][0], acc[v][i][1][1], af[s][i], b[u][s][1]);
-                                    }
-                            }
-                        }
-                    }
-                    pend_round[v] = item.flush_round;
-                    pend_ncol[v] = item.ncol;
-                    pend_nvalid[v] = item.nvalid;
-                }
-                __syncthreads();  // round t done: operands of irreps that ended in it are dead
-                if (t < p.rounds) {
-#pragma unroll
-                    for (int w = 0; w < kSymSlots; ++w) {
-                        if (pend_round[w] >= 0 && pend_round[w] <= t) {
-                            double *orow = xs + (lane >> 2) * P;
-#pragma unroll
-                            for (int fr = 0; fr < 2; ++fr) {
-                                const int j = 8 * fr + 2 * (lane & 3);
-                                const short *nc = coltab + pend_ncol[w] + j;
-                                const int c0 = nc[0], c1 = nc[1];
-                                const bool v0 = j < pend_nvalid[w], v1 = j + 1 < pend_nvalid[w];
-#pragma unroll
-                                for (int i = 0; i < MF; ++i) {
-                                    if (v0) orow[i * 8 * P + c0] = acc[w][i][fr][0];
-                                    if (v1) orow[i * 8 * P + c1] = acc[w][i][fr][1];
-                                }
-                            }
-                            pend_round[w] = -1;
-                        }
-                    }
-                }
+        // ---- irrep products (a short tile of the balanced tail multiplies its present row fragments only)
+        if (rows > 8 * (MF - 1)) {
+            sym_tile_products<MF, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+        } else if (rows <= 8) {
+            sym_tile_products<1, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+        } else {
+            if constexpr (MF > 2) {
+                if (rows <= 16) sym_tile_products<2, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+                else sym_tile_products<MF - 1, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
             }
         }
         __syncthreads();
-        if (!(p.ablate & 2)) sym_tile_butterflies<true, WARPS>(xs, P, R, orb, p.n_orbits);
+        if (!(p.ablate & 2)) sym_tile_butterflies<true, WARPS>(xs, P, rows, orbL, orbS, p.n_orbits, zcol);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes before the bulk stores
         __syncthreads();
         // ---- rows out

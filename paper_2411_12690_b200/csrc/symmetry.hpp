@@ -116,6 +116,68 @@ struct SymTables {
             }
     }
 
+    // Orbit order for the shared-memory butterflies of the fused K1 kernel (sym.cuh): a
+    // half-warp handles `group` consecutive orbits of 16 / group rows, member g of each in
+    // one 8-byte access; with the row pitch = 4 mod 16 doubles and group = 4 that is
+    // conflict-free when the 4 columns differ mod 4 (`mod`). Greedy: every group is filled
+    // with the orbit that adds the fewest same-bank pairs over the 8 members. (The orbit
+    // order is free: src / dst rows move together.)
+    void order_orbits_for_banks(int group = 4, int mod = 4) {
+        if (n_orbits < 2) return;
+        std::vector<int> order, left(n_orbits);
+        for (int o = 0; o < n_orbits; ++o) left[o] = o;
+        int used[8][16];
+        while (!left.empty()) {
+            for (auto &u : used)
+                for (int &v : u) v = 0;
+            for (int slot = 0; slot < group && !left.empty(); ++slot) {
+                size_t best = 0;
+                int best_cost = 1 << 30;
+                for (size_t c = 0; c < left.size(); ++c) {
+                    int cost = 0;
+                    for (int g = 0; g < 8; ++g) {
+                        const int col = src[static_cast<size_t>(left[c]) * 8 + g];
+                        if (col >= 0) cost += used[g][col % mod];
+                    }
+                    if (cost < best_cost) {
+                        best_cost = cost;
+                        best = c;
+                        if (cost == 0) break;
+                    }
+                }
+                const int o = left[best];
+                left.erase(left.begin() + static_cast<long>(best));
+                order.push_back(o);
+                for (int g = 0; g < 8; ++g) {
+                    const int col = src[static_cast<size_t>(o) * 8 + g];
+                    if (col >= 0) ++used[g][col % mod];
+                }
+            }
+        }
+        std::vector<int> s2(src.size()), d2(dst.size());
+        for (int i = 0; i < n_orbits; ++i)
+            for (int g = 0; g < 8; ++g) {
+                s2[static_cast<size_t>(i) * 8 + g] = src[static_cast<size_t>(order[i]) * 8 + g];
+                d2[static_cast<size_t>(i) * 8 + g] = dst[static_cast<size_t>(order[i]) * 8 + g];
+            }
+        src.swap(s2);
+        dst.swap(d2);
+    }
+
+    // Same-bank pairs left per group of orbits, summed over groups and members (0 = conflict-free).
+    int bank_conflicts(int group = 4, int mod = 4) const {
+        int total = 0;
+        for (int o0 = 0; o0 < n_orbits; o0 += group)
+            for (int g = 0; g < 8; ++g) {
+                int cnt[16] = {};
+                for (int o = o0; o < std::min(n_orbits, o0 + group); ++o) {
+                    const int col = src[static_cast<size_t>(o) * 8 + g];
+                    if (col >= 0) total += cnt[col % mod]++;
+                }
+            }
+        return total;
+    }
+
     // In-place unnormalised transform of v[index * stride] over every orbit
     // (plain layout: combination g lands on member g).
     void transform(double *v, size_t stride) const {
@@ -183,6 +245,7 @@ struct SymRomPack {
     double defect_k = 0.0, defect_phi = 0.0;
     std::vector<GemmSeg> k1_segs, k6_segs;
     int k1_tiles_per_m = 0, k6_tiles_per_m = 0;
+    int bank_conflicts_before = 0;  // of the reduced orbit order before order_orbits_for_banks()
     std::vector<double> ks, ps, uts;  // packed K''_r, Phi''_r blocks; H u_T in the fine segmented layout
     std::vector<short> ssrc, sdst;    // reduced orbit tables
     std::vector<int> fsrc;            // fine orbit table: U columns (fine DoFs); Us columns are fine.dst
@@ -210,6 +273,8 @@ struct SymRomPack {
         const int qlen[3] = {static_cast<int>(q[0]), static_cast<int>(q[1]), static_cast<int>(q[2])};
         red.build(qlen, rd, kc);
         if (!red.closed) return false;
+        bank_conflicts_before = red.bank_conflicts();
+        red.order_orbits_for_banks();
         const SymTables &R = red;
         // K'' = H K H S^-1
         std::vector<double> k2 = kp;

@@ -157,6 +157,8 @@ extern "C" int sym_host_check(const uint32_t *q, const int *cells, int n, int n_
         out[7] = span <= 1 ? std::sqrt(nf / den) : -1.0;
         out[8] = fk.conflict_quads;  // k-steps whose four columns collide mod 4 (shared-memory bank conflicts)
         out[9] = fk.quads;
+        out[10] = pk.bank_conflicts_before;  // same-bank pairs of the butterflies' orbit order, natural / reordered
+        out[11] = R.bank_conflicts();
     }
     // K6
     std::vector<double> Us(F.ld, 0.0), U(n_fine, 0.0);
