@@ -356,6 +356,7 @@ struct tsv_ctx {
     // int8 (Ozaki) K1: digit planes of the X panel
     int oz_s = 0;            // digits per value (0 = DMMA K1)
     int graph_oz_s = 0;      // K1 variant baked into the captured graph
+    const double *graph_xlo = nullptr;  // compensated-x vector baked into the captured graph
     long long oz_brows = 0;  // K rows padded to the N tiles
     DevBuf<int8_t> oz_a;
     DevBuf<int> oz_ea;
@@ -2132,6 +2133,19 @@ struct tsv_ctx {
         }
     }
 
+    // Compensated x (x + xlo, TwoSum in the update kernel) for the Schwarz loop; TSV_COMP_X=0: plain x.
+    bool comp_x_active() {
+        if (pre_kind != TSV_PRECOND_SCHWARZ2 || small_pcg_active()) return false;
+        const char *e = std::getenv("TSV_COMP_X");
+        if (e && *e == '0') return false;
+        if (xlo.count != x.count) {
+            xlo.alloc(x.count);
+            CK(cudaMemsetAsync(xlo.ptr, 0, xlo.count * sizeof(double), stream));
+        }
+        return true;
+    }
+    DevBuf<double> xlo;
+
     CgParams cg_params() {
         CgParams q{};
         q.st = state.ptr;
@@ -2144,6 +2158,7 @@ struct tsv_ctx {
         q.r = r.ptr;
         q.p = p.ptr;
         q.ap = ap.ptr;
+        q.xlo = comp_x_active() ? xlo.ptr : nullptr;
         q.Y = Y.ptr;
         q.X = X.ptr;
         q.precond = pre_kind;
@@ -2272,11 +2287,13 @@ struct tsv_ctx {
 
     void ensure_graph() {
         oz_ensure();
-        if (iter_graph && graph_oz_s == oz_s) return;
+        const double *want_xlo = comp_x_active() ? xlo.ptr : nullptr;
+        if (iter_graph && graph_oz_s == oz_s && graph_xlo == want_xlo) return;
         PhaseTimer pt("graph capture");
         drop_graph();
         set_launch_priorities();
         graph_oz_s = oz_s;
+        graph_xlo = want_xlo;
         CgParams q = cg_params();
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
@@ -2438,6 +2455,11 @@ struct tsv_ctx {
         s.phase = PH_INIT;
         s.tol = tol;
         s.max_it = max_it;
+        if (const char *vm = std::getenv("TSV_VERIFY_MARGIN")) s.verify_margin = std::atof(vm);
+        if (pre_kind == TSV_PRECOND_SCHWARZ2 && !as_split() && !fused_gu() && comp_x_active()) {
+            s.replace_at = 1e-6;
+            if (const char *ra = std::getenv("TSV_REPLACE_AT")) s.replace_at = std::atof(ra);
+        }
         *h_state = s;
         CK(cudaMemcpyAsync(state.ptr, h_state, sizeof(CgState), cudaMemcpyHostToDevice, stream));
         CK(cudaMemsetAsync(X.ptr, 0, X.count * sizeof(double), stream));
@@ -2465,6 +2487,11 @@ struct tsv_ctx {
             CK(cudaMemcpyAsync(h_state, state.ptr, sizeof(CgState), cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
             if (h_state->done != CG_RUNNING) break;
+        }
+        if (q.xlo) {
+            fold_x_kernel<<<static_cast<unsigned>(sm_count) * 4, 256, 0, stream>>>(x.ptr, xlo.ptr, static_cast<long long>(x.count));
+            ++launches;
+            CK(cudaGetLastError());
         }
         return *h_state;
     }

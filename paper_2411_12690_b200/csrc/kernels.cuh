@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, Cfg::MINB) gemm_streamk_f64(Gemm
 // ------------------------------------------------------------------- CG
 // Iteration state on the device (cg_solve control flow, linalg.cpp:292-362).
 enum : int { CG_RUNNING = 0, CG_CONVERGED = 1, CG_NOCONV = 2, CG_BREAKDOWN = 3 };
-enum : int { PH_INIT = 0, PH_NORMAL = 1, PH_RESTART = 2 };
+enum : int { PH_INIT = 0, PH_NORMAL = 1, PH_RESTART = 2, PH_REPLACE = 3 };  // REPLACE: r := b - A x, p kept (Schwarz loop)
 
 struct CgState {
     int done;       // CG_*
@@ -435,6 +435,11 @@ struct CgState {
     int it, best_it, max_it, breakdown_code, restarts;
     double rho, alpha, beta, res, best_res, norm_b, tol, tol_abs;
     double rz_l, rz_c;  // Schwarz: r.z split into the local part and (P^T r).zc
+    double verify_margin;  // Schwarz: the recursive residual asks for the A x check at <= margin * tol |b| (0: 1)
+    // Schwarz loop: one residual replacement (r := b - A x, search direction kept) when the
+    // recursive residual first drops below replace_at |b| (0: never)
+    double replace_at;
+    int replacing, replaced;
     unsigned ticket_a, ticket_b, ticket_c;  // c: side-stream kernels
     unsigned bar_gen;                       // software grid barrier generation (fused kernels)
 };
@@ -452,6 +457,7 @@ struct CgParams {
     const uint8_t *cmask;  // [3][node] constrained
     const double *b;
     double *x, *r, *p, *ap;
+    double *xlo;        // nullable (Schwarz loop): low part of the compensated x = x + xlo
     const double *Y;    // block products
     double *X;          // block-major operand panel
     int precond;        // 0 none, 1 diagonal, 2 3x3 node blocks
@@ -586,9 +592,19 @@ __device__ __forceinline__ void cg_gather_finish(CgState *st, int yx, double tot
         st->phase = PH_NORMAL;
     } else {
         st->res = sqrt(tot);
-        if (st->res <= st->tol_abs) st->done = CG_CONVERGED;
-        else st->restarts += 1;
-        st->phase = PH_RESTART;
+        if (st->res <= st->tol_abs) {
+            st->done = CG_CONVERGED;
+            st->phase = PH_RESTART;
+        } else if (st->replacing) {
+            st->phase = PH_REPLACE;  // mid-solve residual replacement: not a failed check
+        } else {
+            st->restarts += 1;
+            st->phase = PH_RESTART;
+        }
+        if (st->replacing) {
+            st->replacing = 0;
+            st->replaced = 1;
+        }
     }
 }
 
