@@ -15,7 +15,7 @@ prev = [i for i in stress if i < end]
 start = 0
 for i in reversed(prev):
     nxt = rows[i + 1]["Kernel Name"]
-    if not ("stress_kernel" in nxt or "gemm_nt_f64" in nxt or "scatter_vec" in nxt):
+    if not any(k in nxt for k in ("stress_kernel", "gemm_nt_f64", "gemm_seg_f64", "scatter_vec", "sym_fine", "sym_panel", "k6_face")):
         start = i + 1
         break
 acc = collections.OrderedDict()

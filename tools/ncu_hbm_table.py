@@ -42,8 +42,10 @@ def algorithmic_bytes(cfg, N_dofs, nc, ntypes, local_rows):
     return {
         # Y panel (each block copy once) + p (dot) + slots + cmask -> Ap
         "cg_gather_kernel": panel64 + vec + slots + cmask + vec,
-        # x, r read+write; p, Ap read; slots2, cmask; XL32 panel written
-        "as_update_kernel": 4 * vec + 2 * vec + slots + cmask + panel32,
+        # x, xlo, r read+write; p, Ap read; slots2, cmask; XL32 panel written
+        "as_update_kernel": 6 * vec + 2 * vec + slots + cmask + panel32,
+        # irrep K1: X panel in, Y panel out (the K'' fragment streams stay in L2)
+        "sym_k1_fused_kernel": 2 * panel64,
         # r, cmask, lat -> 24 partials per coarse cell
         "as_restrict_kernel": vec + cmask + lat,
         "as_restrict_warp_kernel": vec + cmask + lat,
@@ -105,7 +107,8 @@ def main():
                     f"{alg / t / 1e9:.0f}" if alg else "", f"{alg / t / 1e9 / hbm:.3f}" if alg else "",
                     col(r, "launch__grid_size"), col(r, "launch__registers_per_thread"),
                     col(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
-                    f"{k1_flop / t / 1e12:.1f}" if name == "gemm_nt_f64" else ""])
+                    f"{k1_flop / t / 1e12:.1f}" if name == "gemm_nt_f64" else
+                    (f"{k1_flop / 7.97 / t / 1e12:.1f}" if name == "sym_k1_fused_kernel" and cfg.n == 654 else "")])
 
 
 if __name__ == "__main__":
