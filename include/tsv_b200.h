@@ -87,6 +87,7 @@ typedef struct { /* GlobalSolution (global.hpp:91-96) + device timings */
     double solve_ms;          /* device time of the solve, CUDA events on the context stream */
     double loop_ms;           /* of which the iteration loop (excludes the best-iterate replay) */
     int restarts;             /* true-residual verifications that failed and restarted CG (linalg.cpp:321-330) */
+    int replacements;         /* Schwarz loop: mid-solve residual replacements (r := b - A x, direction kept); 0 or 1 */
     uint64_t kernel_launches; /* kernels launched by this call */
 } tsv_solve_info;
 

@@ -117,6 +117,7 @@ class GlobalSolution:
     kernel_launches: int = 0
     loop_ms: float = 0.0
     restarts: int = 0
+    replacements: int = 0
 
 
 @dataclass
@@ -286,7 +287,8 @@ class GpuGlobalStage:
         u = np.empty(self.index().dof_count) if copy_out else None
         rc = self._L.tsv_solve(self._h, C.byref(o), _p(u), C.byref(info))
         sol = GlobalSolution(u, info.iterations, info.relative_residual, bool(info.direct_fallback),
-                             info.best_iterations, info.solve_ms, info.kernel_launches, info.loop_ms, info.restarts)
+                             info.best_iterations, info.solve_ms, info.kernel_launches, info.loop_ms, info.restarts,
+                             info.replacements)
         if rc == TSV_ENOCONV:
             raise NoConvergence(self._L.tsv_last_error(self._h).decode(), sol)
         self._check(rc, "solve_global")

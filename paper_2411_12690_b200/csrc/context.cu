@@ -2364,6 +2364,7 @@ struct tsv_ctx {
             info->solve_ms = ms;
             info->loop_ms = loop_ms;
             info->restarts = st.restarts;
+            info->replacements = st.replaced;
             info->kernel_launches = launches - l0;
         }
         if (status == TSV_ENOCONV) {

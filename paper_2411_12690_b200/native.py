@@ -46,7 +46,7 @@ class IterOptionsC(C.Structure):
 class SolveInfo(C.Structure):
     _fields_ = [("iterations", C.c_int), ("relative_residual", C.c_double), ("direct_fallback", C.c_int),
                 ("best_iterations", C.c_int), ("solve_ms", C.c_double), ("loop_ms", C.c_double), ("restarts", C.c_int),
-                ("kernel_launches", C.c_uint64)]
+                ("replacements", C.c_int), ("kernel_launches", C.c_uint64)]
 
 
 class PrecondInfo(C.Structure):

@@ -69,3 +69,44 @@ def test_tensor_core_local_solve_matches_fp64(oracle_libs, native_lib, monkeypat
     z32, s32 = out["tf32"]
     assert 0 < rel_l2(z32, z64) <= 2e-3
     assert abs(s32.iterations - s64.iterations) <= max(3, s64.iterations // 10)
+
+
+def test_residual_replacement_and_compensated_x(oracle_libs, native_lib, monkeypatch):
+    """The Schwarz loop's compensated x and its one mid-solve residual
+    replacement (r := b - A x, direction kept) leave the answer within the bar
+    of the reference, with and without them; the replacement is taken exactly
+    once when the recursive residual crosses its threshold, and never with
+    TSV_REPLACE_AT=0 or on the reference's preconditioners."""
+    from conftest import RomObj, ref_rom
+    from paper_2411_12690_b200.api import ArrayLayout, GpuGlobalStage, ReducedOrderModel
+    refpy, _ = oracle_libs
+    cfg = configs.get(1)
+    r = ref_rom(cfg, 0, refpy)
+    sess = refpy.RefSession(r, None, cfg.rows, cfg.cols, delta_t=cfg.delta_t(), bc_mode=1)
+    u_ref, _, _ = sess.iterate(1e-12)
+    for k in ("TSV_REPLACE_AT", "TSV_COMP_X", "TSV_VERIFY_MARGIN"):
+        monkeypatch.delenv(k, raising=False)
+    g = GpuGlobalStage(0)
+    g.set_roms(ReducedOrderModel.from_arrays(RomObj(r), 0))
+    g.set_layout(ArrayLayout(cfg.rows, cfg.cols, cfg.kinds(), cfg.delta_t(), cfg.p, cfg.h))
+    g.set_bc("bottom_pin_321")
+    monkeypatch.setenv("TSV_SMALL_PCG", "0")  # the graph loop (the persistent small-array kernel has no replacement)
+    seen = {}
+    for name, env in (("default", {}), ("early", {"TSV_REPLACE_AT": "1e-3"}), ("never", {"TSV_REPLACE_AT": "0"}),
+                      ("plain_x", {"TSV_COMP_X": "0"})):
+        for k in ("TSV_REPLACE_AT", "TSV_COMP_X"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = g.solve_global(IterOptions(1e-12, 10000, "schwarz2"))
+        assert s.relative_residual <= 1e-12 and rel_l2(s.u, u_ref) <= 1e-10, name
+        seen[name] = (s.iterations, s.restarts, s.replacements)
+    assert seen["default"][2] == 1 and seen["early"][2] == 1
+    assert seen["never"][2] == 0 and seen["plain_x"][2] == 0
+    # the replacement costs no iterations where the check passed anyway
+    assert abs(seen["default"][0] - seen["never"][0]) <= 2
+    for k in ("TSV_REPLACE_AT", "TSV_COMP_X"):
+        monkeypatch.delenv(k, raising=False)
+    sj = g.solve_global(IterOptions(1e-12, 100000, "diagonal"))
+    assert sj.replacements == 0 and rel_l2(sj.u, u_ref) <= 1e-10
+    g.close()
