@@ -337,6 +337,7 @@ struct tsv_ctx {
         DevBuf<double> Xs, Ys, Us;
         // fused K1 (one kernel, sym_k1_fused_kernel)
         bool fused = false;
+        bool pipe = false;  // two row buffers, one CTA per SM (sym_k1_pipe_kernel)
         int f_mf = 2, f_items = 0, f_rounds = 0, f_tiles = 0, f_coltab = 0, f_grid = 0;
         size_t f_smem = 0;
         DevBuf<int4> f_tile_tab;
@@ -582,6 +583,14 @@ struct tsv_ctx {
         if (!sym.k1) return;
         setup_sym_fused(*first);
         if (sym.fused) return;
+        {   // the multi-kernel irrep K1 only on request: its true-residual check runs through the irrep
+            // product in FP64, which does not pass at the large configs (section 3 of DESIGN.md)
+            const char *ef = std::getenv("TSV_SYM_K1_FUSED");
+            if (!(ef && *ef == '0')) {
+                sym.k1 = false;
+                return;
+            }
+        }
         sym.Ys.alloc(B_pad * static_cast<size_t>(sym.lds));
         CK(cudaMemsetAsync(sym.Ys.ptr, 0, sym.Ys.count * sizeof(double), stream));
         // correction operand: D32[kind][NP][KP] (the tc_local layout), one common scale
@@ -650,9 +659,9 @@ struct tsv_ctx {
     // Fused K1 on mirror-symmetric ROMs (sym_k1_fused_kernel): item / column /
     // tile tables. TSV_SYM_K1_FUSED=0 keeps the multi-kernel path (panel
     // passes + segmented GEMM); TSV_SYM_K1_MF=2|3|4 picks 16 / 24 / 32 rows per CTA.
-    template <int MF, int WARPS, int MINB>
+    template <int MF, int WARPS, int MINB, int SLOTS = kSymSlots>
     bool sym_fused_config() {
-        auto kern = sym_k1_fused_kernel<MF, WARPS, MINB>;
+        auto kern = sym_k1_fused_kernel<MF, WARPS, MINB, SLOTS>;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sym.f_smem)) != cudaSuccess) {
             cudaGetLastError();
             return false;
@@ -665,17 +674,32 @@ struct tsv_ctx {
         return true;
     }
 
+    bool sym_pipe_config() {
+        auto kern = sym_k1_pipe_kernel<2, 16>;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sym.f_smem)) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, sym.f_smem));
+        if (occ < 1) return false;
+        sym.f_grid = std::min(sym.f_tiles, occ * sm_count);
+        return true;
+    }
+
     void setup_sym_fused(const RomHost &first) {
         sym.fused = false;
         const char *env = std::getenv("TSV_SYM_K1_FUSED");
         if (env && *env == '0') return;
         const char *emf = std::getenv("TSV_SYM_K1_MF");
         const int mf = emf ? std::atoi(emf) : 2;
-        if (mf < 2 || mf > 4) return;
-        const int warps = mf == 2 ? 8 : 16;
+        if (mf < 1 || mf > 4) return;
+        const char *ep = std::getenv("TSV_SYM_K1_PIPE");
+        sym.pipe = mf == 2 && ep && *ep == '1';
+        const int warps = sym.pipe ? 16 : mf == 1 ? 4 : mf == 2 ? 8 : 16;  // mf = 1: 8 rows, 4 warps, 4 CTAs per SM (experiment)
         const SymK1Pack &pk = first.k1f;
         std::vector<short> flush;
-        if (pk.items.empty() || pk.flush_rounds(warps, flush) > kSymSlots - 1) return;
+        if (pk.items.empty() || pk.flush_rounds(warps, flush) > (mf == 1 ? 3 : kSymSlots) - 1) return;
         std::vector<SymK1Item> items(pk.items.size());
         for (size_t i = 0; i < items.size(); ++i) {
             SymK1Item it{};
@@ -692,7 +716,7 @@ struct tsv_ctx {
         sym.f_items = static_cast<int>(items.size());
         sym.f_rounds = (sym.f_items + warps - 1) / warps;
         sym.f_coltab = static_cast<int>(pk.coltab.size());
-        sym.f_smem = sym_k1_smem(mf, static_cast<int>(ldk), first.sred.n_orbits, sym.f_coltab, sym.f_items);
+        sym.f_smem = (sym.pipe ? sym_k1_pipe_smem : sym_k1_smem)(mf, static_cast<int>(ldk), first.sred.n_orbits, sym.f_coltab, sym.f_items);
         if (sym.f_smem > 227 * 1024) return;
         // row tiles: runs of same-kind M tiles cut into 8 MF rows
         std::vector<int4> tiles;
@@ -705,7 +729,8 @@ struct tsv_ctx {
             t = e;
         }
         sym.f_tiles = static_cast<int>(tiles.size());
-        const bool ok = mf == 2 ? sym_fused_config<2, 8, 2>() : mf == 3 ? sym_fused_config<3, 16, 1>() : sym_fused_config<4, 16, 1>();
+        const bool ok = sym.pipe ? sym_pipe_config() : mf == 1 ? sym_fused_config<1, 4, 4, 3>() : mf == 2 ? sym_fused_config<2, 8, 2>()
+                        : mf == 3 ? sym_fused_config<3, 16, 1>() : sym_fused_config<4, 16, 1>();
         if (!ok) return;
         // Balanced tail: the tiles past the last full wave of the grid are cut into single row
         // fragments (8 rows: half the butterflies and products of a 16-row tile), so the last
@@ -769,7 +794,9 @@ struct tsv_ctx {
         sp.skip_flag = skip;
         sp.tile_counter = tile_counter.ptr;
         if (const char *ab = std::getenv("TSV_SYM_ABLATE")) sp.ablate = std::atoi(ab);
-        if (sym.f_mf == 2) launch_pdl(sym_k1_fused_kernel<2, 8, 2>, sym.f_grid, 256, sym.f_smem, stream, sp);
+        if (sym.pipe) launch_pdl(sym_k1_pipe_kernel<2, 16>, sym.f_grid, 512, sym.f_smem, stream, sp);
+        else if (sym.f_mf == 1) launch_pdl(sym_k1_fused_kernel<1, 4, 4, 3>, sym.f_grid, 128, sym.f_smem, stream, sp);
+        else if (sym.f_mf == 2) launch_pdl(sym_k1_fused_kernel<2, 8, 2>, sym.f_grid, 256, sym.f_smem, stream, sp);
         else if (sym.f_mf == 3) launch_pdl(sym_k1_fused_kernel<3, 16, 1>, sym.f_grid, 512, sym.f_smem, stream, sp);
         else launch_pdl(sym_k1_fused_kernel<4, 16, 1>, sym.f_grid, 512, sym.f_smem, stream, sp);
         ++launches;

@@ -412,19 +412,19 @@ __device__ __forceinline__ void bulk_store_row(void *dst, uint32_t src, uint32_t
 }
 
 // The irrep products of one tile on MF row fragments (the kernel's inner part).
-template <int MF, int WARPS>
+template <int MF, int WARPS, int SLOTS>
 __device__ __forceinline__ void sym_tile_products(const SymK1Params &p, double *xs, int P, const SymK1Item *items,
                                                   const short *coltab, double (&b)[kSymRing][kSymKB][2], const double *bw,
                                                   int stream_chunks) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double acc[kSymSlots][MF][2][2];
-    int pend_round[kSymSlots], pend_ncol[kSymSlots], pend_nvalid[kSymSlots];
+    double acc[SLOTS][MF][2][2];
+    int pend_round[SLOTS], pend_ncol[SLOTS], pend_nvalid[SLOTS];
 #pragma unroll
-    for (int v = 0; v < kSymSlots; ++v) pend_round[v] = -1;
+    for (int v = 0; v < SLOTS; ++v) pend_round[v] = -1;
     const double *arow = xs + (lane >> 2) * P;
-    for (int t0 = 0; t0 < p.rounds; t0 += kSymSlots) {
+    for (int t0 = 0; t0 < p.rounds; t0 += SLOTS) {
 #pragma unroll
-        for (int v = 0; v < kSymSlots; ++v) {
+        for (int v = 0; v < SLOTS; ++v) {
             const int t = t0 + v;
             const int it = t * WARPS + warp;
             if (t < p.rounds && it < p.n_items && !(p.ablate & 4)) {
@@ -478,7 +478,7 @@ __device__ __forceinline__ void sym_tile_products(const SymK1Params &p, double *
             __syncthreads();  // round t done: operands of irreps that ended in it are dead
             if (t < p.rounds) {
 #pragma unroll
-                for (int w = 0; w < kSymSlots; ++w) {
+                for (int w = 0; w < SLOTS; ++w) {
                     if (pend_round[w] >= 0 && pend_round[w] <= t) {
                         double *orow = xs + (lane >> 2) * P;
 #pragma unroll
@@ -501,7 +501,7 @@ __device__ __forceinline__ void sym_tile_products(const SymK1Params &p, double *
     }
 }
 
-template <int MF, int WARPS, int MINB>
+template <int MF, int WARPS, int MINB, int SLOTS = kSymSlots>
 __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Params p) {
     pdl_wait();
     extern __shared__ __align__(16) double sym_smem[];
@@ -578,13 +578,13 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
         __syncthreads();
         // ---- irrep products (a short tile of the balanced tail multiplies its present row fragments only)
         if (rows > 8 * (MF - 1)) {
-            sym_tile_products<MF, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+            sym_tile_products<MF, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
         } else if (rows <= 8) {
-            sym_tile_products<1, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+            sym_tile_products<1, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
         } else {
             if constexpr (MF > 2) {
-                if (rows <= 16) sym_tile_products<2, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
-                else sym_tile_products<MF - 1, WARPS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+                if (rows <= 16) sym_tile_products<2, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+                else sym_tile_products<MF - 1, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
             }
         }
         __syncthreads();
@@ -597,6 +597,131 @@ __global__ void __launch_bounds__(32 * WARPS, MINB) sym_k1_fused_kernel(SymK1Par
             for (int r = 0; r < rows; ++r) bulk_store_row(dst + r * p.ld, smem_u32(xs + r * P), row_bytes);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    pdl_trigger();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&p.tile_counter[1], 1u) == gridDim.x - 1) {
+            p.tile_counter[0] = 0u;
+            p.tile_counter[1] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+// ------------------------------------------------ fused K1, two row buffers
+// The same tile work as sym_k1_fused_kernel with one CTA of WARPS warps per SM
+// and two row buffers: the bulk load of the next tile and the bulk store of
+// the previous one are in flight while this tile's butterflies and products
+// run, so the copies leave the critical path (they are 24 of the ~94 us of
+// the single-buffer kernel at config 3).
+inline size_t sym_k1_pipe_smem(int mf, int ldk, int n_orbits, int n_coltab, int n_items) {
+    return sym_k1_smem(mf, ldk, n_orbits, n_coltab, n_items) + static_cast<size_t>(mf) * 8 * (ldk + 4) * sizeof(double);
+}
+
+template <int MF, int WARPS, int SLOTS = kSymSlots>
+__global__ void __launch_bounds__(32 * WARPS, 1) sym_k1_pipe_kernel(SymK1Params p) {
+    pdl_wait();
+    extern __shared__ __align__(16) double sym_smem[];
+    __shared__ int s_tile;
+    __shared__ __align__(8) uint64_t row_bar[2];
+    constexpr int R = 8 * MF, THREADS = 32 * WARPS;
+    const int P = p.ldk + 4;
+    double *buf[2] = {sym_smem, sym_smem + static_cast<size_t>(R) * P};
+    SymK1Item *items = reinterpret_cast<SymK1Item *>(sym_smem + 2 * static_cast<size_t>(R) * P);
+    short *orbL = reinterpret_cast<short *>(items + p.n_items);
+    short *orbS = orbL + p.n_orbits * 8;
+    short *coltab = orbS + p.n_orbits * 8;
+    const int zcol = p.ldk, sink = p.ldk + 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool skip = (p.done != nullptr && *reinterpret_cast<const volatile int *>(p.done) != 0) ||
+                      (p.skip_flag != nullptr && *reinterpret_cast<const volatile int *>(p.skip_flag) != 0);
+    const uint32_t bar[2] = {smem_u32(&row_bar[0]), smem_u32(&row_bar[1])};
+    const uint32_t row_bytes = static_cast<uint32_t>(p.ldk) * 8u;
+    auto issue_load = [&](int tile, int bi) {  // one thread
+        const int4 tl = p.tiles[tile];
+        mbar_expect_tx(bar[bi], row_bytes * static_cast<uint32_t>(tl.y));
+        const double *src = p.X + static_cast<long long>(tl.x) * p.ld;
+        for (int r = 0; r < tl.y; ++r) bulk_load_row(smem_u32(buf[bi] + r * P), src + r * p.ld, row_bytes, bar[bi]);
+    };
+    int cur = p.n_tiles;
+    if (!skip) {
+        for (int i = tid; i < p.n_items * 4; i += THREADS)
+            reinterpret_cast<int *>(items)[i] = reinterpret_cast<const int *>(p.items)[i];
+        for (int i = tid; i < p.n_orbits * 8; i += THREADS) {
+            const short c = p.orb[i];
+            orbL[i] = c >= 0 ? c : static_cast<short>(zcol);
+            orbS[i] = c >= 0 ? c : static_cast<short>(sink);
+        }
+        for (int r = tid; r < 2 * R; r += THREADS) sym_smem[r * P + zcol] = 0.0;
+        for (int i = tid; i < p.n_coltab; i += THREADS) coltab[i] = p.coltab[i];
+        if (tid == 0) {
+            mbar_init(bar[0], 1);
+            mbar_init(bar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
+            if (s_tile < p.n_tiles) issue_load(s_tile, 0);
+        }
+        __syncthreads();
+        cur = s_tile;
+    }
+    uint32_t phase[2] = {0u, 0u};
+    for (int it = 0; cur < p.n_tiles; ++it) {
+        const int bi = it & 1;
+        double *xs = buf[bi];
+        __syncthreads();  // everyone has read s_tile (cur)
+        if (tid == 0) s_tile = static_cast<int>(atomicAdd(&p.tile_counter[0], 1u));
+        const int4 tl = p.tiles[cur];
+        const int rows = tl.y;
+        const double *Bf = tl.z ? p.Bf[1] : p.Bf[0];
+        double b[kSymRing][kSymKB][2];
+        const double *bw = Bf + static_cast<long long>(warp) * p.rounds * p.cpi * (kSymKB * 64) + lane;
+        const int stream_chunks = p.rounds * p.cpi;
+#pragma unroll
+        for (int u = 0; u < kSymRing - 1; ++u)
+#pragma unroll
+            for (int s = 0; s < kSymKB; ++s) {
+                b[u][s][0] = ldg_nc_volatile(bw + (u * kSymKB + s) * 64);
+                b[u][s][1] = ldg_nc_volatile(bw + (u * kSymKB + s) * 64 + 32);
+            }
+        mbar_wait(bar[bi], phase[bi]);
+        phase[bi] ^= 1u;
+        {   // rows of the last active fragment beyond the tile: zeros
+            const int rpad = (rows + 7) / 8 * 8;
+            for (int i = tid; i < (rpad - rows) * p.ldk; i += THREADS) xs[rows * P + (i / p.ldk) * P + i % p.ldk] = 0.0;
+        }
+        __syncthreads();
+        const int nxt = s_tile;
+        sym_tile_butterflies<false, WARPS>(xs, P, rows, orbL, orbS, p.n_orbits, zcol);
+        // the next tile's rows into the other buffer: its previous tenant's bulk stores were
+        // committed a whole tile ago, their shared-memory reads are long done
+        if (tid == 0 && nxt < p.n_tiles) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            issue_load(nxt, bi ^ 1);
+        }
+        __syncthreads();
+        if (rows > 8 * (MF - 1)) {
+            sym_tile_products<MF, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+        } else if (rows <= 8) {
+            sym_tile_products<1, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+        } else {
+            if constexpr (MF > 2) {
+                if (rows <= 16) sym_tile_products<2, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+                else sym_tile_products<MF - 1, WARPS, SLOTS>(p, xs, P, items, coltab, b, bw, stream_chunks);
+            }
+        }
+        __syncthreads();
+        sym_tile_butterflies<true, WARPS>(xs, P, rows, orbL, orbS, p.n_orbits, zcol);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            double *dst = p.Y + static_cast<long long>(tl.x) * p.ld;
+            for (int r = 0; r < rows; ++r) bulk_store_row(dst + r * p.ld, smem_u32(xs + r * P), row_bytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        cur = nxt;
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     pdl_trigger();

@@ -21,7 +21,7 @@ TOL, U_TOL, S_TOL = 1e-12, 1e-10, 1e-8
 
 
 def stage(roms, rows, cols, kinds, dts, cfg, env, monkeypatch, bc="bottom_pin_321"):
-    for k in ("TSV_SYM", "TSV_SYM_K1", "TSV_SYM_CORR", "TSV_SYM_K1_FUSED", "TSV_SYM_K1_MF", "TSV_K1_VERIFY"):
+    for k in ("TSV_SYM", "TSV_SYM_K1", "TSV_SYM_CORR", "TSV_SYM_K1_FUSED", "TSV_SYM_K1_MF", "TSV_K1_VERIFY", "TSV_SYM_K1_PIPE"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -63,6 +63,7 @@ K1_VARIANTS = {
     "fused16": {"TSV_SYM_K1": "1"},
     "fused24": {"TSV_SYM_K1": "1", "TSV_SYM_K1_MF": "3"},
     "fused32": {"TSV_SYM_K1": "1", "TSV_SYM_K1_MF": "4"},
+    "pipe16": {"TSV_SYM_K1": "1", "TSV_SYM_K1_PIPE": "1"},  # two row buffers, one CTA per SM
     "panels": {"TSV_SYM_K1": "1", "TSV_SYM_K1_FUSED": "0"},
     "fused16_dmma_check": {"TSV_SYM_K1": "1", "TSV_K1_VERIFY": "0"},  # A x of the check on the plain DMMA K1
 }
@@ -73,7 +74,7 @@ def test_irrep_operator_matches_reference_csr(case, monkeypatch, variant):
     cfg, roms, rows, cols, kinds, dts, sess = case
     g = stage(roms, rows, cols, kinds, dts, cfg, K1_VARIANTS[variant], monkeypatch)
     s = g.symmetry()
-    assert s["operator"] and s["fused"] == variant.startswith("fused") and s["correction"] == (variant == "panels")
+    assert s["operator"] and s["fused"] == (variant != "panels") and s["correction"] == (variant == "panels")
     gp = stage(roms, rows, cols, kinds, dts, cfg, {"TSV_SYM": "0"}, monkeypatch)
     rng = np.random.default_rng(5)
     for _ in range(3):
@@ -87,7 +88,7 @@ def test_irrep_operator_matches_reference_csr(case, monkeypatch, variant):
     gp.close()
 
 
-@pytest.mark.parametrize("variant", ["fused16", "fused24", "fused16_dmma_check", "panels"])
+@pytest.mark.parametrize("variant", ["fused16", "fused24", "fused16_dmma_check", "pipe16", "panels"])
 @pytest.mark.parametrize("precond", ["diagonal", "schwarz2"])
 def test_irrep_path_solve_and_recovery_parity(case, monkeypatch, precond, variant):
     cfg, roms, rows, cols, kinds, dts, sess = case
@@ -134,7 +135,7 @@ def test_asymmetric_rom_takes_the_plain_path(case, oracle_libs, monkeypatch):
         return o
 
     r2 = [bent(r) for r in roms]
-    for k in ("TSV_SYM", "TSV_SYM_K1", "TSV_SYM_CORR", "TSV_SYM_K1_FUSED", "TSV_SYM_K1_MF", "TSV_K1_VERIFY"):
+    for k in ("TSV_SYM", "TSV_SYM_K1", "TSV_SYM_CORR", "TSV_SYM_K1_FUSED", "TSV_SYM_K1_MF", "TSV_K1_VERIFY", "TSV_SYM_K1_PIPE"):
         monkeypatch.delenv(k, raising=False)
     monkeypatch.setenv("TSV_SYM_K1", "1")
     g = GpuGlobalStage(0)
