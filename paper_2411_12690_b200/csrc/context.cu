@@ -357,7 +357,7 @@ struct tsv_ctx {
     // int8 (Ozaki) K1: digit planes of the X panel
     int oz_s = 0;            // digits per value (0 = DMMA K1)
     int graph_oz_s = 0;      // K1 variant baked into the captured graph
-    const double *graph_xlo = nullptr;  // compensated-x vector baked into the captured graph
+    const float *graph_xlo = nullptr;  // compensated-x vector baked into the captured graph
     long long oz_brows = 0;  // K rows padded to the N tiles
     DevBuf<int8_t> oz_a;
     DevBuf<int> oz_ea;
@@ -370,6 +370,8 @@ struct tsv_ctx {
     cudaStream_t side = nullptr;                       // Schwarz coarse chain (forked in the graph)
     cudaStream_t copy = nullptr;                       // recovery D2H (overlaps the next chunk)
     cudaEvent_t rec_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // [computed, copied] x 2 staging buffers
+    cudaEvent_t k67_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // [K6 done, K7 done] x 2 U buffers (recover_range)
+    DevBuf<double> U2;                                             // second U chunk buffer
     DevBuf<double> rstage[2];
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
@@ -384,6 +386,8 @@ struct tsv_ctx {
         if (stream) cudaStreamSynchronize(stream);
         if (copy) cudaStreamSynchronize(copy);
         tl_alloc_stream = nullptr;
+        for (auto &e : k67_ev)
+            if (e) cudaEventDestroy(e);
         for (auto &e : rec_ev)
             if (e) cudaEventDestroy(e);
         // streams: own_stream / own_side / own_copy, after the DevBuf members
@@ -2167,11 +2171,11 @@ struct tsv_ctx {
         if (e && *e == '0') return false;
         if (xlo.count != x.count) {
             xlo.alloc(x.count);
-            CK(cudaMemsetAsync(xlo.ptr, 0, xlo.count * sizeof(double), stream));
+            CK(cudaMemsetAsync(xlo.ptr, 0, xlo.count * sizeof(float), stream));
         }
         return true;
     }
-    DevBuf<double> xlo;
+    DevBuf<float> xlo;
 
     CgParams cg_params() {
         CgParams q{};
@@ -2314,7 +2318,7 @@ struct tsv_ctx {
 
     void ensure_graph() {
         oz_ensure();
-        const double *want_xlo = comp_x_active() ? xlo.ptr : nullptr;
+        const float *want_xlo = comp_x_active() ? xlo.ptr : nullptr;
         if (iter_graph && graph_oz_s == oz_s && graph_xlo == want_xlo) return;
         PhaseTimer pt("graph capture");
         drop_graph();
@@ -2690,6 +2694,13 @@ struct tsv_ctx {
             if (points == 8) CK(cudaFuncSetAttribute(stress_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
             else CK(cudaFuncSetAttribute(stress_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         }
+        // Opt-in (TSV_REC_OVERLAP=1): stress evaluation of chunk i on the side stream beside the reconstruction
+        // of chunk i + 1 (two U buffers). Measured on B200 with the irrep K6: no gain (config 3 10.5 vs 10.4 ms,
+        // config 4 10.05 vs 10.08 ms) - the persistent K6 grid and K7 take turns on the SMs.
+        const char *eo = std::getenv("TSV_REC_OVERLAP");
+        const bool overlap = points > 0 && eo && *eo == '1';
+        if (overlap) U2.alloc(chunk_tiles * kBM * ldu);
+        int chunk = 0;
         size_t t = 0;
         while (t < m_tiles) {
             if (!need[t]) { ++t; continue; }
@@ -2697,13 +2708,24 @@ struct tsv_ctx {
             while (t1 < m_tiles && need[t1] && t1 - t < chunk_tiles && tile_kind[t1] == tile_kind[t]) ++t1;
             const int kind = tile_kind[t];
             const RomHost &mk = rom[kind];
-            launch_k6(mk, t, t1, U.ptr, ldu);
+            const int ub = overlap ? (chunk & 1) : 0;
+            double *Uc = ub ? U2.ptr : U.ptr;
+            if (overlap && chunk >= 2) CK(cudaStreamWaitEvent(stream, k67_ev[2 + ub], 0));  // K7 of chunk - 2 has read this buffer
+            launch_k6(mk, t, t1, Uc, ldu);
             if (points > 0) {
-                sp.U = U.ptr;
+                cudaStream_t ks = stream;
+                if (overlap) {
+                    CK(cudaEventRecord(k67_ev[ub], stream));
+                    CK(cudaStreamWaitEvent(side, k67_ev[ub], 0));
+                    ks = side;
+                }
+                sp.U = Uc;
                 sp.j0 = static_cast<int>(t * kBM);
                 dim3 grid(static_cast<unsigned>(m.cells[2]), static_cast<unsigned>((t1 - t) * kBM));
-                if (points == 8) stress_kernel<8><<<grid, kStressThreads, smem, stream>>>(sp);
-                else stress_kernel<1><<<grid, kStressThreads, smem, stream>>>(sp);
+                if (points == 8) stress_kernel<8><<<grid, kStressThreads, smem, ks>>>(sp);
+                else stress_kernel<1><<<grid, kStressThreads, smem, ks>>>(sp);
+                if (overlap) CK(cudaEventRecord(k67_ev[2 + ub], side));
+                ++chunk;
             } else {
                 const int res = -points;
                 CutParams cp{};
@@ -2733,6 +2755,9 @@ struct tsv_ctx {
             ++launches;  // stress or cut plane (launch_k6 counts its own)
             CK(cudaGetLastError());
             t = t1;
+        }
+        if (overlap) {  // join: the context stream continues after the last stress kernels
+            for (int b2 = 0; b2 < std::min(chunk, 2); ++b2) CK(cudaStreamWaitEvent(stream, k67_ev[2 + b2], 0));
         }
     }
 };
@@ -2865,6 +2890,7 @@ int tsv_ctx_create(int device, tsv_ctx **out) {
         ctx->side = ctx->own_side.s;
         ctx->copy = ctx->own_copy.s;
         for (auto &e : ctx->rec_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto &e : ctx->k67_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         {
             // freed temporaries stay in the pool up to 16 GB (no OS round trip per set-up)
             cudaMemPool_t pool;

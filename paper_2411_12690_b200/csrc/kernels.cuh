@@ -457,7 +457,7 @@ struct CgParams {
     const uint8_t *cmask;  // [3][node] constrained
     const double *b;
     double *x, *r, *p, *ap;
-    double *xlo;        // nullable (Schwarz loop): low part of the compensated x = x + xlo
+    float *xlo;         // nullable (Schwarz loop): low part of the compensated x = x + xlo (a few ulps of x: FP32 holds it)
     const double *Y;    // block products
     double *X;          // block-major operand panel
     int precond;        // 0 none, 1 diagonal, 2 3x3 node blocks

@@ -153,7 +153,7 @@ __device__ __forceinline__ double as_update_nodes(const CgParams &q, const AsPar
                     const double t = __dadd_rn(xh, inc), bp = __dsub_rn(t, xh);
                     const double err = __dadd_rn(__dsub_rn(xh, __dsub_rn(t, bp)), __dsub_rn(inc, bp));
                     q.x[dof] = t;
-                    q.xlo[dof] += err;
+                    q.xlo[dof] = static_cast<float>(static_cast<double>(q.xlo[dof]) + err);
                 } else {
                     q.x[dof] += alpha * q.p[dof];
                 }
@@ -161,13 +161,13 @@ __device__ __forceinline__ double as_update_nodes(const CgParams &q, const AsPar
                 q.r[dof] = rv;
             } else if (phase == PH_INIT) {
                 q.x[dof] = 0.0;
-                if (q.xlo) q.xlo[dof] = 0.0;
+                if (q.xlo) q.xlo[dof] = 0.f;
                 rv = q.b[dof];
                 q.r[dof] = rv;
             } else {
                 if (q.xlo) {  // restart from the x the check multiplied: x + xlo rounded once
-                    q.x[dof] += q.xlo[dof];
-                    q.xlo[dof] = 0.0;
+                    q.x[dof] += static_cast<double>(q.xlo[dof]);
+                    q.xlo[dof] = 0.f;
                 }
                 rv = q.r[dof];
             }
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
             for (int c = 0; c < 3; ++c) {
                 const long long dof = static_cast<long long>(c) * N + node;
                 if (q.cmask[dof]) continue;
-                const double v = q.xlo ? q.x[dof] + q.xlo[dof] : q.x[dof];
+                const double v = q.xlo ? q.x[dof] + static_cast<double>(q.xlo[dof]) : q.x[dof];
                 const int co = c * q.nn;
                 if (s.x >= 0) q.X[s.x + co] = v;
                 if (s.y >= 0) q.X[s.y + co] = v;
@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
             const double pn = normal ? zv + beta * q.p[dof] : zv;
             q.p[dof] = pn;
             if (cm) continue;
-            const double v = yx ? (q.xlo ? q.x[dof] + q.xlo[dof] : q.x[dof]) : pn;
+            const double v = yx ? (q.xlo ? q.x[dof] + static_cast<double>(q.xlo[dof]) : q.x[dof]) : pn;
             const int co = c * q.nn;
             if (s.x >= 0) q.X[s.x + co] = v;
             if (s.y >= 0) q.X[s.y + co] = v;
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(256) as_zl_split_kernel(CgParams q, AsParams a
             a.z[dof] = zv;
             part[0] += rv * zv;
             if (cm) continue;
-            const double v = yx ? (q.xlo ? q.x[dof] + q.xlo[dof] : q.x[dof]) : zv;
+            const double v = yx ? (q.xlo ? q.x[dof] + static_cast<double>(q.xlo[dof]) : q.x[dof]) : zv;
             if (s.x >= 0) q.X[s.x + co] = v;
             if (s.y >= 0) q.X[s.y + co] = v;
             if (s.z >= 0) q.X[s.z + co] = v;
@@ -1062,11 +1062,11 @@ __global__ void as_symmetrize_kernel(double *A, int Nc) {
 }
 
 // x += xlo, xlo = 0 (end of a solve with the compensated x).
-__global__ void fold_x_kernel(double *x, double *xlo, long long n) {
+__global__ void fold_x_kernel(double *x, float *xlo, long long n) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        x[i] += xlo[i];
-        xlo[i] = 0.0;
+        x[i] += static_cast<double>(xlo[i]);
+        xlo[i] = 0.f;
     }
 }
 
