@@ -95,6 +95,9 @@ typedef struct { /* device-side timings of the last calls (CUDA events, context 
     double solve_ms, recover_ms;
     double apply_ms_avg;      /* mean K1 (operator apply) launch in the last tsv_profile_apply */
     uint64_t kernel_launches; /* cumulative since tsv_ctx_create */
+    double stress_ms;         /* sum of the K7 (stress kernel) launch times of the last recovery, CUDA events */
+    int stress_launches;      /* K7 launches of the last recovery */
+    int reserved_;
 } tsv_timing;
 
 /* Context. */

@@ -375,6 +375,29 @@ struct tsv_ctx {
     DevBuf<double> rstage[2];
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double last_solve_ms = 0, last_recover_ms = 0, last_apply_ms = 0;
+    // K7 launch times of the last recovery (CUDA events around every stress kernel launch)
+    double last_stress_ms = 0;
+    int last_stress_launches = 0;
+    std::vector<cudaEvent_t> k7_ev;  // [2 * launches] start / stop
+    int k7_used = 0;
+    cudaEvent_t k7_event() {
+        if (k7_used == static_cast<int>(k7_ev.size())) {
+            cudaEvent_t e = nullptr;
+            CK(cudaEventCreate(&e));
+            k7_ev.push_back(e);
+        }
+        return k7_ev[k7_used++];
+    }
+    void collect_stress_times() {  // after the recovery's final synchronize
+        last_stress_ms = 0;
+        last_stress_launches = k7_used / 2;
+        for (int i = 0; i + 1 < k7_used; i += 2) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, k7_ev[i], k7_ev[i + 1]) == cudaSuccess) last_stress_ms += ms;
+            else cudaGetLastError();
+        }
+        k7_used = 0;
+    }
 
     ~tsv_ctx() {
         if (iter_graph) cudaGraphExecDestroy(iter_graph);
@@ -387,6 +410,8 @@ struct tsv_ctx {
         if (copy) cudaStreamSynchronize(copy);
         tl_alloc_stream = nullptr;
         for (auto &e : k67_ev)
+            if (e) cudaEventDestroy(e);
+        for (auto &e : k7_ev)
             if (e) cudaEventDestroy(e);
         for (auto &e : rec_ev)
             if (e) cudaEventDestroy(e);
@@ -2722,8 +2747,10 @@ struct tsv_ctx {
                 sp.U = Uc;
                 sp.j0 = static_cast<int>(t * kBM);
                 dim3 grid(static_cast<unsigned>(m.cells[2]), static_cast<unsigned>((t1 - t) * kBM));
+                CK(cudaEventRecord(k7_event(), ks));
                 if (points == 8) stress_kernel<8><<<grid, kStressThreads, smem, ks>>>(sp);
                 else stress_kernel<1><<<grid, kStressThreads, smem, ks>>>(sp);
+                CK(cudaEventRecord(k7_event(), ks));
                 if (overlap) CK(cudaEventRecord(k67_ev[2 + ub], side));
                 ++chunk;
             } else {
@@ -3395,6 +3422,7 @@ int tsv_recover(tsv_ctx *ctx, int points, uint64_t c0, uint64_t c1, double *out)
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         ctx->last_recover_ms = ms;
+        ctx->collect_stress_times();
         return TSV_OK;
     });
 }
@@ -3413,6 +3441,7 @@ int tsv_recover_resident(tsv_ctx *ctx, int points) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         ctx->last_recover_ms = ms;
+        ctx->collect_stress_times();
         return TSV_OK;
     });
 }
@@ -3450,6 +3479,7 @@ int tsv_cutplane(tsv_ctx *ctx, uint32_t res, double *out) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
         ctx->last_recover_ms = ms;
+        ctx->collect_stress_times();
         return TSV_OK;
     });
 }
@@ -3520,6 +3550,8 @@ int tsv_get_timing(tsv_ctx *ctx, tsv_timing *out) {
         out->recover_ms = ctx->last_recover_ms;
         out->apply_ms_avg = ctx->last_apply_ms;
         out->kernel_launches = ctx->launches;
+        out->stress_ms = ctx->last_stress_ms;
+        out->stress_launches = ctx->last_stress_launches;
         return TSV_OK;
     });
 }

@@ -67,7 +67,8 @@ class RomOut(C.Structure):
 
 class Timing(C.Structure):
     _fields_ = [("solve_ms", C.c_double), ("recover_ms", C.c_double), ("apply_ms_avg", C.c_double),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("stress_ms", C.c_double), ("stress_launches", C.c_int),
+                ("reserved_", C.c_int)]
 
 
 class SymmetryInfo(C.Structure):
