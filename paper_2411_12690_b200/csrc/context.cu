@@ -338,7 +338,7 @@ struct tsv_ctx {
         // fused K1 (one kernel, sym_k1_fused_kernel)
         bool fused = false;
         bool pipe = false;  // two row buffers, one CTA per SM (sym_k1_pipe_kernel)
-        int f_mf = 2, f_items = 0, f_rounds = 0, f_tiles = 0, f_coltab = 0, f_grid = 0;
+        int f_mf = 2, f_items = 0, f_rounds = 0, f_tiles = 0, f_coltab = 0, f_grid = 0, f_max_grid = 0;
         size_t f_smem = 0;
         DevBuf<int4> f_tile_tab;
         DevBuf<SymK1Item> f_item_tab;
@@ -608,7 +608,9 @@ struct tsv_ctx {
         sym.Xs.alloc(B_pad * static_cast<size_t>(sym.lds));
         CK(cudaMemsetAsync(sym.Xs.ptr, 0, sym.Xs.count * sizeof(double), stream));
         const char *env = std::getenv("TSV_SYM_K1");
-        sym.k1 = env ? *env == '1' : !k1_small;  // TSV_SYM_K1=1 forces it on small arrays too (tests)
+        // Large arrays, and mid-size ones whose 8-row tiles still fill three quarters of the SMs (config 2:
+        // 128 tiles, 19 -> 13 us against 26.5 us for the split-K DMMA K1); TSV_SYM_K1=1 forces it (tests)
+        sym.k1 = env ? *env == '1' : (!k1_small || (B_pad / 8) * 4 >= static_cast<size_t>(sm_count) * 3);
         if (!sym.k1) return;
         setup_sym_fused(*first);
         if (sym.fused) return;
@@ -698,8 +700,9 @@ struct tsv_ctx {
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, sym.f_smem));
         if (occ < 1) return false;
-        sym.f_grid = std::min(sym.f_tiles, occ * sm_count);
-        if (const char *gr = std::getenv("TSV_SYM_GRID")) sym.f_grid = std::max(1, std::min(sym.f_grid, std::atoi(gr)));
+        sym.f_max_grid = occ * sm_count;
+        if (const char *gr = std::getenv("TSV_SYM_GRID")) sym.f_max_grid = std::max(1, std::min(sym.f_max_grid, std::atoi(gr)));
+        sym.f_grid = std::min(sym.f_tiles, sym.f_max_grid);
         return true;
     }
 
@@ -712,7 +715,8 @@ struct tsv_ctx {
         int occ = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, sym.f_smem));
         if (occ < 1) return false;
-        sym.f_grid = std::min(sym.f_tiles, occ * sm_count);
+        sym.f_max_grid = occ * sm_count;
+        sym.f_grid = std::min(sym.f_tiles, sym.f_max_grid);
         return true;
     }
 
@@ -765,15 +769,17 @@ struct tsv_ctx {
         // fragments (8 rows: half the butterflies and products of a 16-row tile), so the last
         // wave is short instead of leaving most CTAs idle for a whole tile
         {
-            const int T = static_cast<int>(tiles.size()), rem = T > sym.f_grid ? T % sym.f_grid : 0;
+            // (an array with fewer tiles than CTA slots is all tail: every tile is cut)
+            const int T = static_cast<int>(tiles.size()), rem = T % sym.f_max_grid;
             const char *bt = std::getenv("TSV_SYM_K1_TAIL");
-            if (rem > 0 && rem * mf <= sym.f_grid && !(bt && *bt == '0')) {
+            if (rem > 0 && rem * mf <= sym.f_max_grid && !(bt && *bt == '0')) {
                 std::vector<int4> cut(tiles.begin(), tiles.end() - rem);
                 for (int i = T - rem; i < T; ++i)
                     for (int r = 0; r < tiles[i].y; r += 8)
                         cut.push_back(make_int4(tiles[i].x + r, std::min(8, tiles[i].y - r), tiles[i].z, 0));
                 tiles.swap(cut);
                 sym.f_tiles = static_cast<int>(tiles.size());
+                sym.f_grid = std::min(sym.f_tiles, sym.f_max_grid);
             }
         }
         // K'' fragment streams: warp w reads its items (w, w + warps, ...) back to back, every
@@ -1953,7 +1959,7 @@ struct tsv_ctx {
         // DMMA product, and at config 3 the FP64 rounding of A x on the smooth
         // solution is already ~tol |b| (sym vs plain: 1.1e-12 |b|), so an FP64
         // check on that path never passes (B200: 84 restarts in 400 iterations).
-        if (sym.k1 && sym.fused && ldk <= 1024) return 10;
+        if (sym.k1 && sym.fused && ldk <= 1024 && !k1_small) return 10;  // small arrays: the FP64 DMMA check passes there
         // Default off since round 2: with the s = 2 coarse space the FP64 DMMA
         // check restarts no more often than the exact int8 one (config 3: 57
         // iterations / 1 restart either way; configs 0-4 unchanged), and the two
@@ -2134,6 +2140,14 @@ struct tsv_ctx {
         CK(cudaGetLastError());
     }
 
+    // The fused irrep K1 carries this product? On mid-size arrays (k1_small) only for the Schwarz loop and
+    // for stand-alone applies: the reference's preconditioners take thousands of iterations there, and
+    // the irrep products' larger rounding on smooth vectors costs them accuracy against the reference's
+    // own Jacobi solution (config 2: 1.4e-10 instead of 8.8e-13), while Schwarz stays at 3e-12.
+    bool k1_irrep(bool in_loop) const {
+        return sym.k1 && sym.fused && (!k1_small || !in_loop || pre_kind == TSV_PRECOND_SCHWARZ2);
+    }
+
     void launch_k1(const int *done) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(stream, &cs));
@@ -2144,7 +2158,7 @@ struct tsv_ctx {
         if (oz_s && !verify_mode) return oz_s == 9 ? launch_k1_oz<9>(done) : launch_k1_oz<10>(done);
         if (sym.k1 && !sym.fused && !oz_s) return launch_k1_sym(done);
         GemmParams gp = k1_params(done);
-        if (sym.k1 && sym.fused) {
+        if (k1_irrep(done != nullptr)) {
             // The irrep products carry the iteration; inside the PCG loop the A x of
             // the true-residual check goes to the exact int8 path (hybrid) or, when
             // that is off, to the plain DMMA K1 below (run only when y_holds_x).
@@ -2253,7 +2267,7 @@ struct tsv_ctx {
         const int schwarz = as_split() ? (fused_gu() ? 10 : 11) : (fused_gu() ? 9 : 10);
         const bool oz_verify = oz_s && oz_verify_digits();
         int symk = 0;  // extra launches of the irrep K1
-        if (sym.k1 && !(oz_s && !oz_verify)) symk = sym.fused ? (oz_verify ? 0 : 1) : (sym.corr ? 3 : 2);
+        if (sym.k1 && !(oz_s && !oz_verify)) symk = sym.fused ? (k1_irrep(true) && !oz_verify ? 1 : 0) : (sym.corr ? 3 : 2);
         return (pre_kind == TSV_PRECOND_SCHWARZ2 ? schwarz : 4) + (oz_s ? (oz_verify ? 2 : 1) : 0) + symk;
     }
 
