@@ -126,7 +126,13 @@ inline size_t sym_panel_smem(int n_orbits, int n_plain, int n_seg) {
 }
 
 // Us -> U over the fine-DoF orbits: thread = (orbit, group of kFineRows rows).
-constexpr int kFineRows = 8;
+#ifndef TSV_FINE_ROWS
+#define TSV_FINE_ROWS 8
+#endif
+#ifndef TSV_FINE_UNROLL
+#define TSV_FINE_UNROLL 4
+#endif
+constexpr int kFineRows = TSV_FINE_ROWS;
 struct SymFineParams {
     const double *Us;
     long long ldus;
@@ -154,19 +160,28 @@ __global__ void __launch_bounds__(256) sym_fine_kernel(SymFineParams p) {
         if (s[g] >= 0) f |= g;
     const double sc = f == 7 ? 0.125 : (f == 0 ? 1.0 : ((f & (f - 1)) == 0 ? 0.5 : 0.25));
     const int r0 = blockIdx.y * kFineRows;
-#pragma unroll 2
-    for (int rr = 0; rr < kFineRows; ++rr) {
-        const int row = r0 + rr;
-        if (row >= p.rows) break;
-        const double *in = p.Us + static_cast<long long>(row) * p.ldus;
-        double *out = p.U + static_cast<long long>(row) * p.ldu;
-        double x[8];
+    // TSV_FINE_UNROLL rows per batch: all loads of the batch first (the compiler cannot move a row's
+    // loads above the previous row's stores itself), then the butterflies and the stores
+    constexpr int RB = TSV_FINE_UNROLL;
+    for (int rr = 0; rr < kFineRows; rr += RB) {
+        double x[RB][8];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) x[g] = t[g] >= 0 ? __ldcs(in + t[g]) : 0.0;
-        sym_butterfly(x, f);
+        for (int u = 0; u < RB; ++u) {
+            const int row = min(r0 + rr + u, p.rows - 1);
+            const double *in = p.Us + static_cast<long long>(row) * p.ldus;
 #pragma unroll
-        for (int g = 0; g < 8; ++g)
-            if (s[g] >= 0) out[s[g]] = sc * x[g];
+            for (int g = 0; g < 8; ++g) x[u][g] = t[g] >= 0 ? __ldcs(in + t[g]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RB; ++u) {
+            const int row = r0 + rr + u;
+            if (row >= p.rows) break;
+            double *out = p.U + static_cast<long long>(row) * p.ldu;
+            sym_butterfly(x[u], f);
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                if (s[g] >= 0) out[s[g]] = sc * x[u][g];
+        }
     }
 }
 
