@@ -139,6 +139,38 @@ __device__ __forceinline__ double as_update_nodes(const CgParams &q, const AsPar
     double part = 0.0;
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+        if (phase == PH_NORMAL && q.xlo && a.XL32) {
+            // the hot path with the loads of all three components ahead of the stores (the compiler cannot
+            // hoist them itself: the vectors may alias as far as it knows); same arithmetic as below
+            double xh[3], pv[3], rr[3], av[3];
+            float xl[3];
+            uint8_t cm[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const long long dof = static_cast<long long>(c) * N + node;
+                xh[c] = q.x[dof], pv[c] = q.p[dof], rr[c] = q.r[dof], av[c] = q.ap[dof], xl[c] = q.xlo[dof], cm[c] = q.cmask[dof];
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const long long dof = static_cast<long long>(c) * N + node;
+                const double inc = __dmul_rn(alpha, pv[c]);
+                const double t = __dadd_rn(xh[c], inc), bp = __dsub_rn(t, xh[c]);
+                const double err = __dadd_rn(__dsub_rn(xh[c], __dsub_rn(t, bp)), __dsub_rn(inc, bp));
+                q.x[dof] = t;
+                q.xlo[dof] = static_cast<float>(static_cast<double>(xl[c]) + err);
+                const double rv = rr[c] - alpha * av[c];
+                q.r[dof] = rv;
+                part += rv * rv;
+                if (cm[c]) continue;
+                const int co = c * q.nn;
+                const float f = to_tf32(rv);
+                if (s.x >= 0) a.XL32[s.x + co] = f;
+                if (s.y >= 0) a.XL32[s.y + co] = f;
+                if (s.z >= 0) a.XL32[s.z + co] = f;
+                if (s.w >= 0) a.XL32[s.w + co] = f;
+            }
+            continue;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
