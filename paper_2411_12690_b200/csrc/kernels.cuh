@@ -548,6 +548,31 @@ __device__ __forceinline__ double cg_gather_nodes(const CgParams &q, int yx) {
     double part = 0.0;
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+        if (!yx) {
+            // the hot path with the loads of all three components ahead of the stores (the compiler cannot
+            // hoist them itself: the vectors may alias as far as it knows); same sums in the same order
+            double y[3][4], pv[3];
+            uint8_t cm[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const long long dof = static_cast<long long>(c) * N + node;
+                const int co = c * q.nn;
+                cm[c] = q.cmask[dof];
+                pv[c] = q.p[dof];
+                y[c][0] = s.x >= 0 ? q.Y[s.x + co] : 0.0;
+                y[c][1] = s.y >= 0 ? q.Y[s.y + co] : 0.0;
+                y[c][2] = s.z >= 0 ? q.Y[s.z + co] : 0.0;
+                y[c][3] = s.w >= 0 ? q.Y[s.w + co] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const long long dof = static_cast<long long>(c) * N + node;
+                const double acc = cm[c] ? pv[c] : (((0.0 + y[c][0]) + y[c][1]) + y[c][2]) + y[c][3];
+                q.ap[dof] = acc;
+                part += pv[c] * acc;
+            }
+            continue;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;

@@ -649,6 +649,33 @@ __global__ void __launch_bounds__(256) as_zl_kernel(CgParams q, AsParams a) {
     double part[1] = {0.0};
     for (int node = blockIdx.x * blockDim.x + threadIdx.x; node < N; node += gridDim.x * blockDim.x) {
         const int4 s = reinterpret_cast<const int4 *>(a.slots2)[node];
+        if (a.ZL32) {
+            // the hot path with the loads of all three components ahead of the stores; same sums, same order
+            double rr[3];
+            float zl[3][4];
+            uint8_t cm[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const long long dof = static_cast<long long>(c) * N + node;
+                const int co = c * q.nn;
+                rr[c] = q.r[dof];
+                cm[c] = q.cmask[dof];
+                zl[c][0] = s.x >= 0 ? a.ZL32[s.x + co] : 0.f;
+                zl[c][1] = s.y >= 0 ? a.ZL32[s.y + co] : 0.f;
+                zl[c][2] = s.z >= 0 ? a.ZL32[s.z + co] : 0.f;
+                zl[c][3] = s.w >= 0 ? a.ZL32[s.w + co] : 0.f;
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const long long dof = static_cast<long long>(c) * N + node;
+                const double zv = cm[c] ? rr[c]
+                                        : (((0.0 + static_cast<double>(zl[c][0])) + static_cast<double>(zl[c][1])) +
+                                           static_cast<double>(zl[c][2])) + static_cast<double>(zl[c][3]);
+                a.z[dof] = zv;
+                part[0] += rr[c] * zv;
+            }
+            continue;
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
@@ -741,11 +768,22 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
         const double tz = static_cast<double>(L.z) * rdz;
         const int cx = cell % a.SX, cy = cell / a.SX;
         const int4 s = reinterpret_cast<const int4 *>(q.slots)[node];
+        // loads of all three components ahead of the stores (the compiler cannot hoist them itself)
+        double zl3[3], pold[3], xv3[3];
+        uint8_t cm3[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const long long dof = static_cast<long long>(c) * N + node;
-            double zv = a.z[dof];
-            const bool cm = q.cmask[dof] != 0;
+            zl3[c] = a.z[dof];
+            cm3[c] = q.cmask[dof];
+            pold[c] = normal ? q.p[dof] : 0.0;
+            xv3[c] = yx ? (q.xlo ? q.x[dof] + static_cast<double>(q.xlo[dof]) : q.x[dof]) : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const long long dof = static_cast<long long>(c) * N + node;
+            double zv = zl3[c];
+            const bool cm = cm3[c] != 0;
             double zcoarse = 0.0;  // computed whether or not the DoF is constrained (no cmask -> zc dependency)
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -754,10 +792,10 @@ __global__ void __launch_bounds__(256) as_scatter_kernel(CgParams q, AsParams a,
             }
             if (!cm) zv += zcoarse;
             if (write_z) a.z[dof] = zv;
-            const double pn = normal ? zv + beta * q.p[dof] : zv;
+            const double pn = normal ? zv + beta * pold[c] : zv;
             q.p[dof] = pn;
             if (cm) continue;
-            const double v = yx ? (q.xlo ? q.x[dof] + static_cast<double>(q.xlo[dof]) : q.x[dof]) : pn;
+            const double v = yx ? xv3[c] : pn;
             const int co = c * q.nn;
             if (s.x >= 0) q.X[s.x + co] = v;
             if (s.y >= 0) q.X[s.y + co] = v;
