@@ -383,8 +383,19 @@ inline size_t sym_k1_smem(int mf, int ldk, int n_orbits, int n_coltab, int n_ite
 // unconditionally (a stage over an axis the orbit does not move adds zeros to
 // the present members and only touches absent ones otherwise). INV: scaled by
 // 1 / |orbit|.
+#ifndef TSV_SYM_BF_PAIR
+#define TSV_SYM_BF_PAIR 0
+#endif
+#ifndef TSV_SYM_BF_NOINLINE
+#define TSV_SYM_BF_NOINLINE 0
+#endif
+#if TSV_SYM_BF_NOINLINE
+#define TSV_SYM_BF_ATTR __noinline__
+#else
+#define TSV_SYM_BF_ATTR __forceinline__
+#endif
 template <bool INV, int WARPS>
-__device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int rows, const short *orbL, const short *orbS,
+__device__ TSV_SYM_BF_ATTR void sym_tile_butterflies(double *xs, int P, int rows, const short *orbL, const short *orbS,
                                                      int n_orbits, int zcol) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = lane >> 2;  // 0..7: row within a block of 8
@@ -403,6 +414,29 @@ __device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int rows
             for (int g = 0; g < 8; ++g) members += ml[g] != zcol;
             s = 1.0 / static_cast<double>(members);  // 1, 2, 4 or 8 members: exact
         }
+#if TSV_SYM_BF_PAIR
+        // two rows per pass with all loads ahead of the stores (the compiler cannot reorder them itself)
+        int r = r0;
+        for (; r + 8 < rows; r += 16) {
+            double *row = xs + r * P, *row2 = row + 8 * P;
+            double x[8], y[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) x[g] = row[ml[g]], y[g] = row2[ml[g]];
+            sym_butterfly(x, 7);
+            sym_butterfly(y, 7);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) row[ms[g]] = INV ? s * x[g] : x[g], row2[ms[g]] = INV ? s * y[g] : y[g];
+        }
+        if (r < rows) {
+            double *row = xs + r * P;
+            double x[8];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) x[g] = row[ml[g]];
+            sym_butterfly(x, 7);
+#pragma unroll
+            for (int g = 0; g < 8; ++g) row[ms[g]] = INV ? s * x[g] : x[g];
+        }
+#else
 #pragma unroll 2
         for (int r = r0; r < rows; r += 8) {
             double *row = xs + r * P;
@@ -413,6 +447,7 @@ __device__ __forceinline__ void sym_tile_butterflies(double *xs, int P, int rows
 #pragma unroll
             for (int g = 0; g < 8; ++g) row[ms[g]] = INV ? s * x[g] : x[g];
         }
+#endif
     }
 }
 
