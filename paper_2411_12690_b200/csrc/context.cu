@@ -1817,25 +1817,26 @@ struct tsv_ctx {
         return !(v && *v == '0');
     }
 
-    void launch_coarse_chain(const CgParams &q, const AsParams &a) {
+    void launch_coarse_chain(const CgParams &q, const AsParams &a, cudaStream_t cs = nullptr) {
+        if (!cs) cs = side;
         if (getenv_flag("TSV_AS_RESTRICT_CTA"))
-            launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 3 * kRestrictGroup, 0, side, q, a);
+            launch_pdl(as_restrict_kernel, as2.ncells * kAsSplit, 3 * kRestrictGroup, 0, cs, q, a);
         else
             launch_pdl(as_restrict_warp_kernel, (as2.ncells + kRestrictWarps - 1) / kRestrictWarps, 32 * kRestrictWarps, 0,
-                       side, q, a);
-        launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, side, q, a);
+                       cs, q, a);
+        launch_pdl(as_coarse_rhs_kernel, (as2.Nc + 255) / 256, 256, 0, cs, q, a);
         if (as2.sym_nt) {
             const int ntiles = as2.sym_nt * (as2.sym_nt + 1) / 2;
             // one 64 x 64 tile per CTA (a fixed grid walking tiles with a
             // register prefetch of the next tile measured slower: 0.655 vs
             // 0.620 ms per iteration at config 3)
-            launch_pdl(as_coarse_symv_kernel, ntiles, 128, 0, side, q, a, static_cast<const float *>(as2.sym_tiles.ptr),
+            launch_pdl(as_coarse_symv_kernel, ntiles, 128, 0, cs, q, a, static_cast<const float *>(as2.sym_tiles.ptr),
                        as2.sym_nt, as2.sym_part.ptr);
-            launch_pdl(as_coarse_symv_reduce_kernel, as2.sym_nt, kSymRedG * kSymT, 0, side, q, a, as2.sym_nt,
+            launch_pdl(as_coarse_symv_reduce_kernel, as2.sym_nt, kSymRedG * kSymT, 0, cs, q, a, as2.sym_nt,
                        static_cast<const double *>(as2.sym_part.ptr));
         } else {
-            as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, side>>>(q, a);
-            as_coarse_dot_kernel<<<1, 1024, 0, side>>>(q, a);
+            as_coarse_gemv_kernel<<<(as2.Nc + kGemvRows - 1) / kGemvRows, 256, 0, cs>>>(q, a);
+            as_coarse_dot_kernel<<<1, 1024, 0, cs>>>(q, a);
         }
     }
 
@@ -1855,10 +1856,19 @@ struct tsv_ctx {
             // gather -> fork {coarse chain on P^T r - alpha P^T Ap} || {update
             // -> local solves -> z_l} -> join
             launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
-            CK(cudaEventRecord(ev_fork, stream));
-            CK(cudaStreamWaitEvent(side, ev_fork, 0));
             AsParams ae = a;
             ae.rc_recur = 1;
+            if (getenv_flag("TSV_AS_SERIAL")) {
+                // experiment: the coarse chain in line on the context stream (no fork / join)
+                launch_coarse_chain(q, ae, stream);
+                launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+                launch_local_solve();
+                launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+                launches += 7;
+                return;
+            }
+            CK(cudaEventRecord(ev_fork, stream));
+            CK(cudaStreamWaitEvent(side, ev_fork, 0));
             launch_coarse_chain(q, ae);
             CK(cudaEventRecord(ev_join, side));
             launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);

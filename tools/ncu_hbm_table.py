@@ -42,8 +42,8 @@ def algorithmic_bytes(cfg, N_dofs, nc, ntypes, local_rows):
     return {
         # Y panel (each block copy once) + p (dot) + slots + cmask -> Ap
         "cg_gather_kernel": panel64 + vec + slots + cmask + vec,
-        # x, xlo, r read+write; p, Ap read; slots2, cmask; XL32 panel written
-        "as_update_kernel": 6 * vec + 2 * vec + slots + cmask + panel32,
+        # x, r read+write (8 B), xlo read+write (4 B); p, Ap read; slots2, cmask; XL32 panel written
+        "as_update_kernel": 5 * vec + 2 * vec + slots + cmask + panel32,
         # irrep K1: X panel in, Y panel out (the K'' fragment streams stay in L2)
         "sym_k1_fused_kernel": 2 * panel64,
         # r, cmask, lat -> 24 partials per coarse cell
