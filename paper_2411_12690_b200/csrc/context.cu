@@ -1855,15 +1855,15 @@ struct tsv_ctx {
         if (with_gather && !fused_gu() && early_coarse()) {
             // gather -> fork {coarse chain on P^T r - alpha P^T Ap} || {update
             // -> local solves -> z_l} -> join
-            launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
+            launch_pdl(cg_gather_kernel, wave_grid(cg_gather_kernel), kVecThreads, 0, stream, q);
             AsParams ae = a;
             ae.rc_recur = 1;
             if (getenv_flag("TSV_AS_SERIAL")) {
                 // experiment: the coarse chain in line on the context stream (no fork / join)
                 launch_coarse_chain(q, ae, stream);
-                launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+                launch_pdl(as_update_kernel, wave_grid(as_update_kernel), kVecThreads, 0, stream, q, a);
                 launch_local_solve();
-                launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+                launch_pdl(as_zl_kernel, wave_grid(as_zl_kernel), kVecThreads, 0, stream, q, a);
                 launches += 7;
                 return;
             }
@@ -1871,9 +1871,9 @@ struct tsv_ctx {
             CK(cudaStreamWaitEvent(side, ev_fork, 0));
             launch_coarse_chain(q, ae);
             CK(cudaEventRecord(ev_join, side));
-            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+            launch_pdl(as_update_kernel, wave_grid(as_update_kernel), kVecThreads, 0, stream, q, a);
             launch_local_solve();
-            launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+            launch_pdl(as_zl_kernel, wave_grid(as_zl_kernel), kVecThreads, 0, stream, q, a);
             CK(cudaStreamWaitEvent(stream, ev_join, 0));
             launches += 7;
             return;
@@ -1882,12 +1882,12 @@ struct tsv_ctx {
         // per-cell partials) measured slower at config 3: 80 us vs 47 + 34 us
         // with the restriction off the critical path on the side stream.
         if (!with_gather) {
-            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+            launch_pdl(as_update_kernel, wave_grid(as_update_kernel), kVecThreads, 0, stream, q, a);
         } else if (fused_gu()) {
             launch_pdl(as_gather_update_kernel, gu_grid(), kVecThreads, 0, stream, q, a);
         } else {
-            launch_pdl(cg_gather_kernel, cg_grid(), kVecThreads, 0, stream, q);
-            launch_pdl(as_update_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+            launch_pdl(cg_gather_kernel, wave_grid(cg_gather_kernel), kVecThreads, 0, stream, q);
+            launch_pdl(as_update_kernel, wave_grid(as_update_kernel), kVecThreads, 0, stream, q, a);
         }
         // fork: the coarse chain (cell sums of the restriction -> coarse rhs
         // -> coarse solve, HBM and latency bound) runs on a side stream beside
@@ -1899,7 +1899,7 @@ struct tsv_ctx {
         CK(cudaEventRecord(ev_join, side));
         launch_local_solve();
         // the local part of z (and r.z_l) while the coarse chain finishes
-        launch_pdl(as_zl_kernel, cg_grid(), kVecThreads, 0, stream, q, a);
+        launch_pdl(as_zl_kernel, wave_grid(as_zl_kernel), kVecThreads, 0, stream, q, a);
         CK(cudaStreamWaitEvent(stream, ev_join, 0));
         launches += 7;
     }
@@ -1911,7 +1911,7 @@ struct tsv_ctx {
             // node-parallel (a warp-per-coarse-cell variant that loads the
             // cell's 24 coarse values once measured slower: 68.8 vs 54 us at
             // config 3, too few threads in flight for an HBM-bound pass)
-            launch_pdl(as_scatter_kernel, cg_grid(), kVecThreads, 0, stream, q, a, write_z);
+            launch_pdl(as_scatter_kernel, wave_grid(as_scatter_kernel), kVecThreads, 0, stream, q, a, write_z);
         } else {
             launch_pdl(cg_scatter_kernel, cg_grid(), kVecThreads, 0, stream, q);
         }
@@ -1923,6 +1923,23 @@ struct tsv_ctx {
     // CG vector kernels: fixed grid (grid-stride), so the per-CTA partials
     // and their fixed-order sum stay small and deterministic.
     unsigned cg_grid() const { return std::min<unsigned>(vec_grid(), static_cast<unsigned>(sm_count) * 8u); }
+    // One resident wave of a grid-stride vector kernel: its occupancy x SMs (capped by cg_grid()). With the
+    // three components' loads hoisted the kernels use 40-74 registers, so 8 CTAs per SM no longer fit and the
+    // fixed grid of 8 per SM ran 1.3-2.7 waves with a partly filled last one. TSV_VEC_WAVE=0: the old grid.
+    template <class K>
+    unsigned wave_grid(K kern) {
+        static const bool off = [] { const char *e = std::getenv("TSV_VEC_WAVE"); return e && *e == '0'; }();
+        if (off) return cg_grid();
+        const void *key = reinterpret_cast<const void *>(kern);
+        for (const auto &kv : wave_cache)
+            if (kv.first == key) return std::min(kv.second, cg_grid());
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kVecThreads, 0));
+        const unsigned g = static_cast<unsigned>(std::max(1, occ) * sm_count);
+        wave_cache.emplace_back(key, g);
+        return std::min(g, cg_grid());
+    }
+    std::vector<std::pair<const void *, unsigned>> wave_cache;
 
     void launch_scatter(const double *v, int mode) {
         scatter_vec_kernel<<<vec_grid(), kVecThreads, 0, stream>>>(static_cast<int>(nodes), static_cast<int>(n / 3), slots.ptr, cmask.ptr, v,
