@@ -401,7 +401,10 @@ __global__ void __launch_bounds__(3 * kRestrictGroup) as_restrict_kernel(CgParam
 // A single wave of short-lived warps instead of thousands of CTAs whose
 // block reductions dominate (as_restrict_kernel); TSV_AS_RESTRICT_CTA=1
 // keeps the CTA-per-cell kernel.
-constexpr int kRestrictWarps = 8;
+#ifndef TSV_RESTRICT_WARPS
+#define TSV_RESTRICT_WARPS 8
+#endif
+constexpr int kRestrictWarps = TSV_RESTRICT_WARPS;
 __global__ void __launch_bounds__(32 * kRestrictWarps) as_restrict_warp_kernel(CgParams q, AsParams a) {
     pdl_wait();
     if (*reinterpret_cast<volatile int *>(&q.st->done)) return;
